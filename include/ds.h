@@ -1,0 +1,237 @@
+/*
+ * ds.h — C ABI of the B200-native DistServe KV-cache data path (libds.so).
+ *
+ * DistServe (arXiv 2401.09670) disaggregates LLM serving into a prefill
+ * instance and a decoding instance. The prefill instance
+ * computes the prompt's KV cache and keeps it in its GPU memory;
+ * the decoding instance receives "the KV caches and the first output token"
+ * by pulling them into paged memory (PagedAttention, P:251,
+ * P:407) and then generates one token per step.
+ * Tensor parallelism divides the heads; KV moves only between
+ * corresponding layers.
+ *
+ * This header is the whole boundary of the hot path:
+ *   a1  ds_block_table      page allocation / block tables (host)
+ *   a2+a3 ds_prefill_attn   causal prefill attention + paged K/V write
+ *   a4  ds_kv_pack          gather pages of a head slice into a staging buffer
+ *   a5  ds_kv_migrate       pack -> NCCL send/recv over NVLink -> unpack
+ *   a6  ds_kv_unpack        scatter a staging buffer into pages
+ *   a7+a8 ds_decode_attn    decode append + split-K paged attention + combine
+ *
+ * Conventions (all entry points):
+ *  - Every call returns ds_status and never throws or aborts. On a non-OK
+ *    status, ds_last_error() returns thread-local text describing it.
+ *  - Validation is synchronous and happens before any launch; a rejected call
+ *    launches nothing and changes nothing.
+ *  - GPU work is stream-ordered and asynchronous on the caller's `stream`
+ *    (a cudaStream_t passed as void*; NULL = legacy default stream). Device
+ *    faults surface at the caller's next synchronisation.
+ *  - Pointers are DEVICE pointers unless the name ends in `_h` (host).
+ *  - All K/V/Q/O tensors are bf16 (2 bytes); there is no dtype or arch dispatch:
+ *    bf16 and sm_100a only. There is no CPU fallback: without a usable sm_100
+ *    device every compute entry point returns DS_ERR_CUDA.
+ *  - Ownership: all tensors, tables, workspaces and staging buffers are owned
+ *    by the caller (allocated with torch in the Python layer). The library owns
+ *    only the opaque handles (ds_pool, ds_comm) and cached TMA descriptors.
+ *    Pointer arguments are not retained after the call's stream work completes.
+ *
+ * KV cache layout (one allocation per pool and rank; reading R3/R-layout):
+ *   base[L_loc][2 (0=K,1=V)][num_blocks][n_loc][block_size=16][head_dim]
+ * A page (layer, kv, block, head) is 16*head_dim*2 bytes contiguous (4 KiB at
+ * head_dim 128); a head range inside one block is contiguous.
+ */
+#ifndef DS_H_
+#define DS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DS_OK = 0,
+  DS_ERR_INVALID_ARG = 1, /* argument validation failed; nothing launched */
+  DS_ERR_UNSUPPORTED = 2, /* valid request this build does not implement */
+  DS_ERR_NO_BLOCKS = 3,   /* pool too small; all-or-nothing, nothing changed */
+  DS_ERR_CUDA = 4,        /* CUDA runtime/launch error or no sm_100 device */
+  DS_ERR_NCCL = 5,        /* NCCL error (text from ncclGetErrorString) */
+  DS_ERR_STATE = 6        /* handle misuse (destroyed, wrong role, ...) */
+} ds_status;
+
+/* Thread-local description of the last non-OK status on this thread. */
+const char *ds_last_error(void);
+
+/* Library/build identification: e.g. "libds sm_100a nccl 2.28.9". */
+const char *ds_build_info(void);
+
+/* Caller-owned paged KV pool of one rank (layout above). */
+typedef struct {
+  void *base;         /* device, 16-B aligned */
+  int32_t num_layers; /* L_loc  (PP stage's layer count)  */
+  int32_t num_blocks; /* pages per (layer, kv, head)              */
+  int32_t num_heads;  /* n_loc  (TP rank's head count)     */
+  int32_t block_size; /* must be 16 (BASELINE.json)               */
+  int32_t head_dim;   /* 64 or 128                                */
+} ds_kv_cache;
+
+/* ======================================================================
+ * a1 — page allocation and block tables (host, synchronous).
+ * PagedAttention-style fixed-size pages with a per-request logical->physical
+ * map. The paper gives no policy; ours (reading R13):
+ * lowest free id first, sequences in argument order, blocks in logical order.
+ * ==================================================================== */
+typedef struct ds_pool_s *ds_pool; /* library-owned free set of [0, num_blocks) */
+
+ds_status ds_pool_create(int32_t num_blocks, ds_pool *out_h);
+ds_status ds_pool_destroy(ds_pool pool);
+/* Number of free pages (host). */
+ds_status ds_pool_num_free(ds_pool pool, int32_t *num_free_h);
+
+enum { DS_BT_APPEND = 0, DS_BT_FREE = 1 };
+
+/* op = DS_BT_APPEND: for each sequence s grow from cur_lens_h[s] to
+ *   cur_lens_h[s] + add_lens_h[s] tokens; a page is taken for each logical block
+ *   in [ceil(cur/bs), ceil((cur+add)/bs)) and written to table_h[s][block].
+ *   ALLOC is APPEND from cur_len 0. Entries below ceil(cur/bs) are not touched.
+ *   If the pool cannot satisfy the whole call: DS_ERR_NO_BLOCKS, nothing changes
+ *   (SPEC CapacityError / up-front admission).
+ * op = DS_BT_FREE: return the ceil(cur_lens_h[s]/bs) pages of each row to the
+ *   pool and set those entries to -1 (add_lens_h ignored, may be NULL).
+ * table_h: host int32 [num_seqs][max_blocks_per_seq], row-major, -1 = no page.
+ * block_size must be 16. num_seqs == 0 is a no-op. num_free_h may be NULL.
+ * Errors: DS_ERR_INVALID_ARG (negative lengths, ceil(len/bs) > max_blocks_per_seq,
+ * FREE of an id that is not allocated), DS_ERR_NO_BLOCKS. */
+ds_status ds_block_table(ds_pool pool, int32_t op, int32_t num_seqs,
+                         const int32_t *cur_lens_h, const int32_t *add_lens_h,
+                         int32_t *table_h, int32_t max_blocks_per_seq,
+                         int32_t block_size, int32_t *num_free_h);
+
+/* ======================================================================
+ * a2 + a3 — prefill causal attention of one layer, fused paged K/V write.
+ * For every sequence r, head h, row i < l_r (§2.1; App. A:
+ * attention only among the tokens of the same request; readings R1, R2):
+ *   out[i] = sum_{j<=i} softmax_j(scale * q[i].k[j]) v[j]
+ * and (a3, "KV caches ... saved in GPU memory"):
+ *   cache[layer][K][block_table[r][t/16]][h][t%16][:] = k[t][h][:]   (and V)
+ *
+ * q, k, v, out : bf16 [T][n_loc][head_dim], packed varlen (token-major), T =
+ *                total_tokens = cu_seqlens[num_seqs] (host value; sizes the TMA
+ *                descriptors); row stride n_loc*head_dim.
+ * cu_seqlens   : device int32 [num_seqs+1], cu[0]=0, non-decreasing, every
+ *                length >= 1; max_seqlen >= every length (host value).
+ * block_table  : device int32 [num_seqs][max_blocks_per_seq]; row r must hold
+ *                ceil(l_r/16) valid page ids (from ds_block_table APPEND).
+ * cache        : host pointer to the pool descriptor; cache->num_heads must
+ *                equal n_loc. layer in [0, num_layers).
+ * Numerics: bf16 inputs, fp32 S and O accumulation (tcgen05, TMEM), online
+ * base-2 softmax, P rounded to bf16 for the P.V MMA, bf16 output (RNE).
+ * Page slots at positions >= l_r in a sequence's last page are unspecified.
+ * Errors: DS_ERR_INVALID_ARG (head_dim not 64/128, block_size != 16, misaligned
+ * pointers, num_seqs < 0, max_seqlen < 1, layer out of range), DS_ERR_CUDA. */
+ds_status ds_prefill_attn(const void *q, const void *k, const void *v, void *out,
+                          const int32_t *cu_seqlens, int32_t num_seqs, int32_t total_tokens,
+                          int32_t max_seqlen,
+                          const ds_kv_cache *cache, int32_t layer,
+                          const int32_t *block_table, int32_t max_blocks_per_seq,
+                          float softmax_scale, void *stream);
+
+/* ======================================================================
+ * a7 + a8 — one decode step of one layer ("generates subsequent tokens
+ * one at a time"; P:237 batching; P:696-698 memory-bound decode attention).
+ * Reading R9: the new token's K/V are appended at position c = cache_lens[b]
+ * BEFORE attending, so the step attends c+1 tokens and equals row c of
+ * prefill over those c+1 tokens:
+ *   (i)  cache[layer][K][bt[b][c/16]][h][c%16] = k_new[b][h]   (and V)
+ *   (ii) out[b][h] = sum_{j<=c} softmax_j(scale * q[b][h].k[j]) v[j]
+ * q, k_new, v_new, out : bf16 [num_seqs][n_loc][head_dim].
+ * block_table : device int32 [num_seqs][max_blocks_per_seq]; row b must already
+ *               hold the page for position c (ds_block_table APPEND by 1).
+ * cache_lens  : device int32 [num_seqs], c >= 0; max_cache_len >= every c
+ *               (host value; sizes the split-K grid).
+ * workspace   : device scratch of >= ds_decode_workspace_bytes(...) bytes, 16-B
+ *               aligned, caller-owned, contents need no initialisation.
+ * The split-K partials (m, l, o) are merged with a log-sum-exp combine (a8).
+ * Errors: DS_ERR_INVALID_ARG, DS_ERR_CUDA. */
+size_t ds_decode_workspace_bytes(int32_t num_seqs, int32_t n_loc, int32_t head_dim,
+                                 int32_t max_cache_len);
+ds_status ds_decode_attn(const void *q, const void *k_new, const void *v_new, void *out,
+                         const ds_kv_cache *cache, int32_t layer,
+                         const int32_t *block_table, int32_t max_blocks_per_seq,
+                         const int32_t *cache_lens, int32_t num_seqs, int32_t max_cache_len,
+                         float softmax_scale, void *workspace, size_t workspace_bytes,
+                         void *stream);
+
+/* ======================================================================
+ * a4 / a6 — pack and unpack whole pages of a head slice (KV migration, P:363:
+ * only between corresponding layers; P:633 head shards; reading R14: whole
+ * pages move, slots beyond a sequence's length are unspecified).
+ * Staging layout (contiguous, bf16):
+ *   staging[layer - layer_begin][kv][i][0:head_count][16][head_dim]
+ *     = cache[layer][kv][block_ids[i]][head_begin : head_begin+head_count]
+ * for i in [0, num_blocks), layer in [layer_begin, layer_begin+layer_count).
+ * Size: ds_kv_staging_bytes(...) = layer_count*2*num_blocks*head_count*16*head_dim*2.
+ * block_ids: device int32 [num_blocks] (logical order of the requests' pages).
+ * ds_kv_unpack is the inverse scatter into the destination cache's pages.
+ * Errors: DS_ERR_INVALID_ARG (ranges, sizes, alignment), DS_ERR_CUDA. */
+size_t ds_kv_staging_bytes(const ds_kv_cache *cache, int32_t layer_count,
+                           int32_t num_blocks, int32_t head_count);
+ds_status ds_kv_pack(const ds_kv_cache *cache, int32_t layer_begin, int32_t layer_count,
+                     const int32_t *block_ids, int32_t num_blocks, int32_t head_begin,
+                     int32_t head_count, void *staging, size_t staging_bytes, void *stream);
+ds_status ds_kv_unpack(const ds_kv_cache *cache, int32_t layer_begin, int32_t layer_count,
+                       const int32_t *block_ids, int32_t num_blocks, int32_t head_begin,
+                       int32_t head_count, const void *staging, size_t staging_bytes,
+                       void *stream);
+
+/* ======================================================================
+ * a5 — KV migration prefill rank -> decode rank over NVLink with NCCL p2p
+ * ("NCCL ... and asynchronous CudaMemcpy", P:265 sizing, P:382 pull,
+ * P:512 transfer time). The communicator is library-owned and bootstrapped
+ * by the caller exchanging the 128-byte unique id (e.g. via torch's store).
+ * ==================================================================== */
+typedef struct ds_comm_s *ds_comm;
+
+/* Writes a 128-byte ncclUniqueId into id_h (host). */
+ds_status ds_comm_get_unique_id(void *id_h);
+/* Collective over the nranks processes; binds to the current CUDA device. */
+ds_status ds_comm_init(const void *id_h, int32_t nranks, int32_t rank, ds_comm *out_h);
+ds_status ds_comm_destroy(ds_comm comm);
+
+enum { DS_MIGRATE_SEND = 0, DS_MIGRATE_RECV = 1, DS_MIGRATE_SELF = 2 };
+
+/* Move whole pages of (layers [layer_begin, +layer_count), head slice
+ * [head_begin, +head_count), block_ids[0..num_blocks)) from a prefill rank to
+ * a decode rank. Both sides call it with equal layer_count, num_blocks and
+ * head_count (their block ids and head offsets may differ):
+ *  role SEND (prefill side, `peer` = decode rank): ds_kv_pack into the staging
+ *       buffer chunk by chunk, ncclSend each chunk.
+ *  role RECV (decode side, `peer` = prefill rank): ncclRecv each chunk into
+ *       staging, ds_kv_unpack it into this rank's pages.
+ *  role SELF (one rank plays both, N=1 loopback through NCCL): `cache` is the
+ *       source, `dst_cache`/`dst_block_ids`/`dst_head_begin` the destination;
+ *       the staging buffer holds two halves (send and receive side).
+ * Chunking: the (layer, kv, block) page-rows are moved in chunks of about
+ * 64 MiB (at least one row of head_count pages) through a 2-slot ring in the
+ * staging buffer (2 send + 2 receive slots for SELF); the pack of chunk k+1
+ * overlaps the transfer of chunk k, the unpack of chunk k the transfer of k+1.
+ * The chunking depends only on (head_dim, layer_count, num_blocks, head_count),
+ * so both ends agree. staging_bytes must be >= ds_kv_migrate_staging_bytes().
+ * The caller's stream is ordered after the whole migration on return of the
+ * stream work; NCCL runs on a library-owned side stream.
+ * A peer mismatch of counts is undefined behaviour (NCCL hangs or errors).
+ * Errors: DS_ERR_INVALID_ARG, DS_ERR_STATE, DS_ERR_NCCL, DS_ERR_CUDA. */
+size_t ds_kv_migrate_staging_bytes(const ds_kv_cache *cache, int32_t role, int32_t layer_count,
+                                   int32_t num_blocks, int32_t head_count);
+ds_status ds_kv_migrate(ds_comm comm, int32_t role, int32_t peer, const ds_kv_cache *cache,
+                        int32_t layer_begin, int32_t layer_count, const int32_t *block_ids,
+                        int32_t num_blocks, int32_t head_begin, int32_t head_count,
+                        const ds_kv_cache *dst_cache, const int32_t *dst_block_ids,
+                        int32_t dst_head_begin, void *staging, size_t staging_bytes,
+                        void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DS_H_ */

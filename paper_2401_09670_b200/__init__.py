@@ -1,0 +1,321 @@
+"""Python binding of libds.so — the B200-native DistServe KV-cache data path.
+
+Thin ctypes marshalling over the C ABI in include/ds.h: every function keeps
+the C name and only turns torch tensors into (pointer, size) arguments; all
+compute runs in the library's sm_100a kernels. PyTorch is used for device
+memory, streams and process groups only.
+
+There is no fallback of any kind: if libds.so is missing or cannot load, the
+import raises; on a device that is not sm_100, every compute call raises
+DSError (DS_ERR_CUDA).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libds.so")
+
+DS_OK, DS_ERR_INVALID_ARG, DS_ERR_UNSUPPORTED, DS_ERR_NO_BLOCKS, DS_ERR_CUDA, DS_ERR_NCCL, DS_ERR_STATE = range(7)
+DS_BT_APPEND, DS_BT_FREE = 0, 1
+DS_MIGRATE_SEND, DS_MIGRATE_RECV, DS_MIGRATE_SELF = 0, 1, 2
+BLOCK_SIZE = 16
+
+# every symbol include/ds.h declares (checked by tests/test_abi.py)
+EXPORTED = (
+    "ds_last_error", "ds_build_info", "ds_pool_create", "ds_pool_destroy", "ds_pool_num_free",
+    "ds_block_table", "ds_prefill_attn", "ds_decode_workspace_bytes", "ds_decode_attn",
+    "ds_kv_staging_bytes", "ds_kv_pack", "ds_kv_unpack", "ds_comm_get_unique_id", "ds_comm_init",
+    "ds_comm_destroy", "ds_kv_migrate_staging_bytes", "ds_kv_migrate",
+)
+
+
+class DSError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"ds status {status}: {msg}")
+        self.status = status
+
+
+class ds_kv_cache(ctypes.Structure):
+    _fields_ = [("base", ctypes.c_void_p), ("num_layers", ctypes.c_int32),
+                ("num_blocks", ctypes.c_int32), ("num_heads", ctypes.c_int32),
+                ("block_size", ctypes.c_int32), ("head_dim", ctypes.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2401_09670_b200.build` "
+                          "(there is no fallback implementation)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
+    f32, cache_p = ctypes.c_float, ctypes.POINTER(ds_kv_cache)
+    sig = {
+        "ds_last_error": ([], ctypes.c_char_p),
+        "ds_build_info": ([], ctypes.c_char_p),
+        "ds_pool_create": ([i32, ctypes.POINTER(P)], ctypes.c_int),
+        "ds_pool_destroy": ([P], ctypes.c_int),
+        "ds_pool_num_free": ([P, ctypes.POINTER(i32)], ctypes.c_int),
+        "ds_block_table": ([P, i32, i32, P, P, P, i32, i32, ctypes.POINTER(i32)], ctypes.c_int),
+        "ds_prefill_attn": ([P, P, P, P, P, i32, i32, i32, cache_p, i32, P, i32, f32, P], ctypes.c_int),
+        "ds_decode_workspace_bytes": ([i32, i32, i32, i32], sz),
+        "ds_decode_attn": ([P, P, P, P, cache_p, i32, P, i32, P, i32, i32, f32, P, sz, P], ctypes.c_int),
+        "ds_kv_staging_bytes": ([cache_p, i32, i32, i32], sz),
+        "ds_kv_pack": ([cache_p, i32, i32, P, i32, i32, i32, P, sz, P], ctypes.c_int),
+        "ds_kv_unpack": ([cache_p, i32, i32, P, i32, i32, i32, P, sz, P], ctypes.c_int),
+        "ds_comm_get_unique_id": ([P], ctypes.c_int),
+        "ds_comm_init": ([P, i32, i32, ctypes.POINTER(P)], ctypes.c_int),
+        "ds_comm_destroy": ([P], ctypes.c_int),
+        "ds_kv_migrate_staging_bytes": ([cache_p, i32, i32, i32, i32], sz),
+        "ds_kv_migrate": ([P, i32, i32, cache_p, i32, i32, P, i32, i32, i32, cache_p, P, i32, P, sz, P],
+                          ctypes.c_int),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes, fn.restype = args, res
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def ds_last_error() -> str:
+    return _lib.ds_last_error().decode()
+
+
+def ds_build_info() -> str:
+    return _lib.ds_build_info().decode()
+
+
+def _check(status: int):
+    if status != DS_OK:
+        raise DSError(status, ds_last_error())
+
+
+# --------------------------------------------------------------------- helpers
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int | None:
+    torch = _torch()
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dev(t, dtype, name):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (there is no CPU path)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return t
+
+
+class KVCache:
+    """Caller-owned paged KV pool of one rank: bf16 [L][2][num_blocks][n][16][D]."""
+
+    def __init__(self, tensor):
+        torch = _torch()
+        _dev(tensor, torch.bfloat16, "cache")
+        if tensor.dim() != 6 or tensor.shape[1] != 2 or tensor.shape[4] != BLOCK_SIZE:
+            raise ValueError("cache must be [L][2][num_blocks][n][16][head_dim]")
+        self.tensor = tensor
+        L, _, NB, n, bs, D = tensor.shape
+        self.desc = ds_kv_cache(tensor.data_ptr(), L, NB, n, bs, D)
+
+    @classmethod
+    def empty(cls, layers, num_blocks, heads, head_dim, device="cuda"):
+        torch = _torch()
+        return cls(torch.empty((layers, 2, num_blocks, heads, BLOCK_SIZE, head_dim),
+                               dtype=torch.bfloat16, device=device))
+
+    @property
+    def layers(self):
+        return self.desc.num_layers
+
+    @property
+    def num_blocks(self):
+        return self.desc.num_blocks
+
+    @property
+    def heads(self):
+        return self.desc.num_heads
+
+    @property
+    def head_dim(self):
+        return self.desc.head_dim
+
+    def ref(self):
+        return ctypes.byref(self.desc)
+
+
+# --------------------------------------------------------------------- a1
+class Pool:
+    """ds_pool: library-owned free set of page ids [0, num_blocks)."""
+
+    def __init__(self, num_blocks: int):
+        h = ctypes.c_void_p()
+        _check(_lib.ds_pool_create(num_blocks, ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.ds_pool_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    @property
+    def num_free(self) -> int:
+        n = ctypes.c_int32()
+        _check(_lib.ds_pool_num_free(self._h, ctypes.byref(n)))
+        return n.value
+
+
+def ds_block_table(pool: Pool, op: int, cur_lens, add_lens, table: np.ndarray,
+                   block_size: int = BLOCK_SIZE) -> int:
+    """Host block-table op (APPEND / FREE). `table` is an int32 numpy array
+    [num_seqs][max_blocks_per_seq] updated in place; returns the free count."""
+    cur = np.ascontiguousarray(cur_lens, dtype=np.int32)
+    add = None if add_lens is None else np.ascontiguousarray(add_lens, dtype=np.int32)
+    if table.dtype != np.int32 or not table.flags.c_contiguous or table.ndim != 2:
+        raise ValueError("table must be a C-contiguous int32 [num_seqs][max_blocks] array")
+    if table.shape[0] != len(cur) or (add is not None and len(add) != len(cur)):
+        raise ValueError("table rows, cur_lens and add_lens must agree")
+    nf = ctypes.c_int32()
+    _check(_lib.ds_block_table(pool._h, op, len(cur), cur.ctypes.data, None if add is None else add.ctypes.data,
+                               table.ctypes.data, table.shape[1], block_size, ctypes.byref(nf)))
+    return nf.value
+
+
+# --------------------------------------------------------------------- a2 + a3
+def ds_prefill_attn(q, k, v, out, cu_seqlens, max_seqlen: int, cache: KVCache, layer: int,
+                    block_table, softmax_scale: float, stream=None, total_tokens: int | None = None):
+    torch = _torch()
+    for t, nm in ((q, "q"), (k, "k"), (v, "v"), (out, "out")):
+        _dev(t, torch.bfloat16, nm)
+    _dev(cu_seqlens, torch.int32, "cu_seqlens")
+    _dev(block_table, torch.int32, "block_table")
+    T = q.shape[0] if total_tokens is None else total_tokens
+    if q.dim() != 3 or q.shape[1] != cache.heads or q.shape[2] != cache.head_dim:
+        raise ValueError("q must be [T][n_loc][head_dim] matching the cache")
+    for t in (k, v, out):
+        if t.shape != q.shape:
+            raise ValueError("q, k, v, out must have the same shape")
+    _check(_lib.ds_prefill_attn(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                cu_seqlens.data_ptr(), cu_seqlens.numel() - 1, T, max_seqlen,
+                                cache.ref(), layer, block_table.data_ptr(), block_table.shape[1],
+                                softmax_scale, _stream(stream)))
+
+
+# --------------------------------------------------------------------- a7 + a8
+def ds_decode_workspace_bytes(num_seqs: int, n_loc: int, head_dim: int, max_cache_len: int) -> int:
+    return int(_lib.ds_decode_workspace_bytes(num_seqs, n_loc, head_dim, max_cache_len))
+
+
+def ds_decode_attn(q, k_new, v_new, out, cache: KVCache, layer: int, block_table, cache_lens,
+                   max_cache_len: int, softmax_scale: float, workspace, stream=None):
+    torch = _torch()
+    for t, nm in ((q, "q"), (k_new, "k_new"), (v_new, "v_new"), (out, "out")):
+        _dev(t, torch.bfloat16, nm)
+    _dev(block_table, torch.int32, "block_table")
+    _dev(cache_lens, torch.int32, "cache_lens")
+    B = q.shape[0]
+    if q.dim() != 3 or q.shape[1] != cache.heads or q.shape[2] != cache.head_dim:
+        raise ValueError("q must be [B][n_loc][head_dim] matching the cache")
+    ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(),
+                                                            workspace.numel() * workspace.element_size())
+    _check(_lib.ds_decode_attn(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), out.data_ptr(),
+                               cache.ref(), layer, block_table.data_ptr(), block_table.shape[1],
+                               cache_lens.data_ptr(), B, max_cache_len, softmax_scale, ws_ptr,
+                               ws_bytes, _stream(stream)))
+
+
+# --------------------------------------------------------------------- a4 / a6
+def ds_kv_staging_bytes(cache: KVCache, layer_count: int, num_blocks: int, head_count: int) -> int:
+    return int(_lib.ds_kv_staging_bytes(cache.ref(), layer_count, num_blocks, head_count))
+
+
+def _nbytes(t):
+    return t.numel() * t.element_size()
+
+
+def ds_kv_pack(cache: KVCache, layer_begin: int, layer_count: int, block_ids, head_begin: int,
+               head_count: int, staging, stream=None):
+    torch = _torch()
+    _dev(block_ids, torch.int32, "block_ids")
+    _check(_lib.ds_kv_pack(cache.ref(), layer_begin, layer_count, block_ids.data_ptr(), block_ids.numel(),
+                           head_begin, head_count, staging.data_ptr(), _nbytes(staging), _stream(stream)))
+
+
+def ds_kv_unpack(cache: KVCache, layer_begin: int, layer_count: int, block_ids, head_begin: int,
+                 head_count: int, staging, stream=None):
+    torch = _torch()
+    _dev(block_ids, torch.int32, "block_ids")
+    _check(_lib.ds_kv_unpack(cache.ref(), layer_begin, layer_count, block_ids.data_ptr(), block_ids.numel(),
+                             head_begin, head_count, staging.data_ptr(), _nbytes(staging), _stream(stream)))
+
+
+# --------------------------------------------------------------------- a5
+def ds_comm_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.ds_comm_get_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """ds_comm: library-owned NCCL communicator (+ side stream) for KV migration."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int):
+        if len(unique_id) != 128:
+            raise ValueError("unique_id must be 128 bytes")
+        h = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(unique_id, 128)
+        _check(_lib.ds_comm_init(buf, nranks, rank, ctypes.byref(h)))
+        self._h, self.rank, self.nranks = h, rank, nranks
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.ds_comm_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+
+def ds_comm_init(unique_id: bytes, nranks: int, rank: int) -> Comm:
+    return Comm(unique_id, nranks, rank)
+
+
+def ds_kv_migrate_staging_bytes(cache: KVCache, role: int, layer_count: int, num_blocks: int,
+                                head_count: int) -> int:
+    return int(_lib.ds_kv_migrate_staging_bytes(cache.ref(), role, layer_count, num_blocks, head_count))
+
+
+def ds_kv_migrate(comm: Comm, role: int, peer: int, cache: KVCache, layer_begin: int, layer_count: int,
+                  block_ids, head_begin: int, head_count: int, staging, dst_cache: KVCache | None = None,
+                  dst_block_ids=None, dst_head_begin: int = 0, stream=None):
+    torch = _torch()
+    _dev(block_ids, torch.int32, "block_ids")
+    if dst_block_ids is not None:
+        _dev(dst_block_ids, torch.int32, "dst_block_ids")
+    _check(_lib.ds_kv_migrate(comm._h, role, peer, cache.ref(), layer_begin, layer_count,
+                              block_ids.data_ptr(), block_ids.numel(), head_begin, head_count,
+                              None if dst_cache is None else dst_cache.ref(), _ptr(dst_block_ids),
+                              dst_head_begin, staging.data_ptr(), _nbytes(staging), _stream(stream)))

@@ -1,0 +1,50 @@
+// kernels.h — internal launch interface between the C ABI (api.cu) and the
+// sm_100a kernels. Not part of the public boundary (include/ds.h is).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace ds {
+
+// a7 + a8
+struct DecodeArgs {
+  const uint16_t *q, *k_new, *v_new;  // bf16 [B][n][D]
+  void *out;                          // bf16 [B][n][D]
+  const uint16_t *cache;              // pool base [L][2][NB][n][16][D]
+  const int32_t *block_table;         // [B][max_blocks]
+  const int32_t *cache_lens;          // [B]
+  float *workspace;                   // [B][n][splits][D+2]
+  int32_t layer, num_blocks, n_loc, max_blocks, num_seqs;
+  int32_t num_splits, pages_per_split;
+  float scale_log2;  // softmax_scale * log2(e)
+};
+cudaError_t launch_decode(const DecodeArgs &a, int head_dim, cudaStream_t stream);
+
+// a4 / a6: page rows <-> staging
+struct KvCopyArgs {
+  uint16_t *cache;          // pool base
+  uint16_t *staging;        // [rows][head_count][16][D]
+  const int32_t *block_ids; // [num_blocks]
+  int32_t layer_begin, num_blocks_sel, head_begin, head_count;
+  int32_t pool_blocks, n_loc, head_dim;
+  int64_t row_begin, row_end;  // rows of (layer, kv, i) to copy, staging row r at r - row_begin
+};
+cudaError_t launch_kv_copy(const KvCopyArgs &a, bool pack, cudaStream_t stream);
+
+// a2 + a3
+struct PrefillArgs {
+  void *out;                   // bf16 [T][n][D]
+  const int32_t *cu_seqlens;   // [B+1]
+  const int32_t *block_table;  // [B][max_blocks]
+  int32_t num_seqs, n_loc, max_blocks, num_q_tiles;
+  int32_t layer, num_blocks;   // cache layer / pool pages
+  float scale_log2;
+};
+cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
+                           const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
+                           cudaStream_t stream);
+size_t prefill_smem_bytes(int head_dim);
+
+}  // namespace ds

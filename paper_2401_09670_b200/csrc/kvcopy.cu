@@ -1,0 +1,81 @@
+// kvcopy.cu — a4 pack / a6 unpack of whole KV pages for migration.
+//
+// KV moves only between corresponding layers and TP ranks own
+// contiguous head ranges (reading R11), so for every (layer, kv, block)
+// the head slice [head_begin, head_begin+head_count) is ONE contiguous run of
+// head_count pages (4 KiB each at head_dim 128) in the pool layout
+// [L][2][NB][n][16][D]. Pack/unpack is therefore a gather/scatter of
+// contiguous rows: staging row r = (layer, kv, i) <-> pool row
+// (layer_begin+layer, kv, block_ids[i], head_begin..).
+//
+// HBM-bound copy: 256-thread CTAs, each thread moves 4 x 16 B per iteration
+// (all loads issued before the stores), grid-stride over (row, 16 KiB segment)
+// work items; grid = a multiple of the 148 SMs.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ds {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+constexpr int kSegBytes = kThreads * kUnroll * 16;  // 16 KiB per work item
+
+DS_DEVICE uint4 ld_stream(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+template <bool kPack>
+__global__ void __launch_bounds__(kThreads) kv_copy_kernel(const KvCopyArgs a) {
+  const int64_t page_bytes = 16LL * a.head_dim * 2;
+  const int64_t row_bytes = page_bytes * a.head_count;
+  const int64_t segs_per_row = (row_bytes + kSegBytes - 1) / kSegBytes;
+  const int64_t rows = a.row_end - a.row_begin;
+  const int64_t items = rows * segs_per_row;
+  const int64_t kv_stride = (int64_t)a.pool_blocks * a.n_loc * page_bytes;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t rr = it / segs_per_row, seg = it % segs_per_row;
+    const int64_t r = a.row_begin + rr;
+    const int64_t i = r % a.num_blocks_sel;
+    const int64_t kv = (r / a.num_blocks_sel) & 1;
+    const int64_t layer = a.layer_begin + r / (2LL * a.num_blocks_sel);
+    const int64_t blk = a.block_ids[i];
+    char *pool_row = reinterpret_cast<char *>(a.cache) + (2 * layer + kv) * kv_stride +
+                     (blk * a.n_loc + a.head_begin) * page_bytes;
+    char *stage_row = reinterpret_cast<char *>(a.staging) + rr * row_bytes;
+    const char *src = kPack ? pool_row : stage_row;
+    char *dst = kPack ? stage_row : pool_row;
+    const int64_t base = seg * kSegBytes;
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t off = base + ((int64_t)u * kThreads + threadIdx.x) * 16;
+      if (off < row_bytes) v[u] = ld_stream(reinterpret_cast<const uint4 *>(src + off));
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t off = base + ((int64_t)u * kThreads + threadIdx.x) * 16;
+      if (off < row_bytes) *reinterpret_cast<uint4 *>(dst + off) = v[u];
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_kv_copy(const KvCopyArgs &a, bool pack, cudaStream_t stream) {
+  const int64_t row_bytes = 16LL * a.head_dim * 2 * a.head_count;
+  const int64_t items = (a.row_end - a.row_begin) * ((row_bytes + kSegBytes - 1) / kSegBytes);
+  if (items <= 0) return cudaSuccess;
+  int grid = (int)(items < 148LL * 8 ? items : 148LL * 8);
+  if (pack)
+    kv_copy_kernel<true><<<grid, kThreads, 0, stream>>>(a);
+  else
+    kv_copy_kernel<false><<<grid, kThreads, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace ds

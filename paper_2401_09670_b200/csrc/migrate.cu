@@ -1,0 +1,231 @@
+// migrate.cu — a5: KV migration prefill rank -> decode rank with NCCL p2p.
+//
+// PAPER.md P:407 (NCCL across nodes, asynchronous cudaMemcpy within a node —
+// "avoids blocking the GPU computation during transmission"), P:265 (1.13 GB per
+// OPT-66B 512-token request), P:382 (decode instances *pull* KV when they have
+// memory; the prefill GPU's memory is the queue buffer), P:363 (only between
+// corresponding layers), P:633 (TP head shards).
+//
+// On B200 every GPU of the node reaches every peer at full NVLink-5 bandwidth
+// through NVSwitch, so one two-sided ncclSend/ncclRecv per chunk is the whole
+// protocol. Pages are gathered (a4) into a chunk ring in the staging buffer on
+// the caller's stream while NCCL moves the previous chunk on a library-owned
+// side stream; the receiver scatters (a6) chunk k while chunk k+1 is in flight.
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+
+#include "../../include/ds.h"
+#include "internal.h"
+#include "kernels.h"
+
+namespace ds {
+ds_status kv_copy_checked(const ds_kv_cache *cache, int32_t layer_begin, int32_t layer_count,
+                          const int32_t *block_ids, int32_t num_blocks, int32_t head_begin,
+                          int32_t head_count, void *staging, size_t staging_bytes,
+                          int64_t row_begin, int64_t row_end, bool pack, cudaStream_t stream,
+                          const char *W);
+}  // namespace ds
+
+using namespace ds;
+
+struct ds_comm_s {
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 0, device = -1;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_a[2] = {nullptr, nullptr};  // recorded on the caller's stream
+  cudaEvent_t ev_b[2] = {nullptr, nullptr};  // recorded on the side (NCCL) stream
+};
+
+namespace {
+constexpr int64_t kChunkTarget = 64ll << 20;  // bytes per transfer chunk
+
+#define DS_CUDA(call, W)                                        \
+  do {                                                          \
+    cudaError_t e_ = (call);                                    \
+    if (e_ != cudaSuccess)                                      \
+      return fail(DS_ERR_CUDA, "%s: %s", W, cudaGetErrorString(e_)); \
+  } while (0)
+#define DS_NCCL(call, W)                                        \
+  do {                                                          \
+    ncclResult_t r_ = (call);                                   \
+    if (r_ != ncclSuccess)                                      \
+      return fail(DS_ERR_NCCL, "%s: %s", W, ncclGetErrorString(r_)); \
+  } while (0)
+
+int64_t chunk_rows_for(int64_t row_bytes, int64_t rows) {
+  int64_t c = kChunkTarget / row_bytes;
+  if (c < 1) c = 1;
+  if (c > rows) c = rows;
+  return c;
+}
+}  // namespace
+
+extern "C" const char *ds_build_info(void) {
+  static char buf[128];
+  int v = 0;
+  ncclGetVersion(&v);
+  snprintf(buf, sizeof buf, "libds sm_100a nccl %d.%d.%d", v / 10000, (v / 100) % 100, v % 100);
+  return buf;
+}
+
+extern "C" size_t ds_kv_migrate_staging_bytes(const ds_kv_cache *cache, int32_t role,
+                                              int32_t layer_count, int32_t num_blocks,
+                                              int32_t head_count) {
+  if (!cache || layer_count <= 0 || num_blocks <= 0 || head_count <= 0) return 0;
+  const int64_t row_bytes = (int64_t)head_count * 16 * cache->head_dim * 2;
+  const int64_t rows = (int64_t)layer_count * 2 * num_blocks;
+  const int64_t slots = role == DS_MIGRATE_SELF ? 4 : 2;
+  return (size_t)(slots * chunk_rows_for(row_bytes, rows) * row_bytes);
+}
+
+extern "C" ds_status ds_comm_get_unique_id(void *id_h) {
+  if (!id_h) return fail(DS_ERR_INVALID_ARG, "ds_comm_get_unique_id: NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  DS_NCCL(ncclGetUniqueId(&id), "ds_comm_get_unique_id");
+  memcpy(id_h, &id, sizeof id);
+  return DS_OK;
+}
+
+extern "C" ds_status ds_comm_init(const void *id_h, int32_t nranks, int32_t rank, ds_comm *out_h) {
+  const char *W = "ds_comm_init";
+  if (!id_h || !out_h || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(DS_ERR_INVALID_ARG, "%s: bad arguments", W);
+  ds_comm c = new (std::nothrow) ds_comm_s();
+  if (!c) return fail(DS_ERR_INVALID_ARG, "%s: out of host memory", W);
+  ncclUniqueId id;
+  memcpy(&id, id_h, sizeof id);
+  c->rank = rank;
+  c->nranks = nranks;
+  cudaGetDevice(&c->device);
+  ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(DS_ERR_NCCL, "%s: %s", W, ncclGetErrorString(r));
+  }
+  cudaError_t e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaEventCreateWithFlags(&c->ev_a[i], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_b[i], cudaEventDisableTiming);
+  }
+  if (e != cudaSuccess) {
+    ds_comm_destroy(c);
+    return fail(DS_ERR_CUDA, "%s: %s", W, cudaGetErrorString(e));
+  }
+  *out_h = c;
+  return DS_OK;
+}
+
+extern "C" ds_status ds_comm_destroy(ds_comm c) {
+  if (!c) return fail(DS_ERR_STATE, "ds_comm_destroy: NULL");
+  if (c->side) cudaStreamSynchronize(c->side);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_start) cudaEventDestroy(c->ev_start);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_a[i]) cudaEventDestroy(c->ev_a[i]);
+    if (c->ev_b[i]) cudaEventDestroy(c->ev_b[i]);
+  }
+  delete c;
+  return DS_OK;
+}
+
+extern "C" ds_status ds_kv_migrate(ds_comm comm, int32_t role, int32_t peer,
+                                   const ds_kv_cache *cache, int32_t layer_begin,
+                                   int32_t layer_count, const int32_t *block_ids,
+                                   int32_t num_blocks, int32_t head_begin, int32_t head_count,
+                                   const ds_kv_cache *dst_cache, const int32_t *dst_block_ids,
+                                   int32_t dst_head_begin, void *staging, size_t staging_bytes,
+                                   void *stream) {
+  const char *W = "ds_kv_migrate";
+  if (!comm || !comm->comm) return fail(DS_ERR_STATE, "%s: invalid communicator", W);
+  if (role != DS_MIGRATE_SEND && role != DS_MIGRATE_RECV && role != DS_MIGRATE_SELF)
+    return fail(DS_ERR_INVALID_ARG, "%s: bad role", W);
+  if (role == DS_MIGRATE_SELF) peer = comm->rank;
+  if (peer < 0 || peer >= comm->nranks) return fail(DS_ERR_INVALID_ARG, "%s: peer out of range", W);
+  if (role != DS_MIGRATE_SELF && peer == comm->rank)
+    return fail(DS_ERR_INVALID_ARG, "%s: SEND/RECV to self; use DS_MIGRATE_SELF", W);
+  if (!cache) return fail(DS_ERR_INVALID_ARG, "%s: NULL cache", W);
+  if (layer_count < 0 || num_blocks < 0 || head_count < 0)
+    return fail(DS_ERR_INVALID_ARG, "%s: negative count", W);
+  if (role == DS_MIGRATE_SELF) {
+    if (!dst_cache || !dst_block_ids) return fail(DS_ERR_INVALID_ARG, "%s: SELF needs dst_cache/dst_block_ids", W);
+    if (dst_cache->head_dim != cache->head_dim)
+      return fail(DS_ERR_INVALID_ARG, "%s: head_dim differs between source and destination", W);
+  }
+  {  // validate both ends up front so a rejected call launches nothing
+    const ds_kv_cache *ends[2] = {cache, role == DS_MIGRATE_SELF ? dst_cache : cache};
+    const int32_t h0s[2] = {head_begin, role == DS_MIGRATE_SELF ? dst_head_begin : head_begin};
+    for (int e = 0; e < 2; ++e) {
+      const ds_kv_cache *c = ends[e];
+      if (!c->base || c->block_size != 16 || (c->head_dim != 64 && c->head_dim != 128))
+        return fail(DS_ERR_INVALID_ARG, "%s: bad cache descriptor", W);
+      if (layer_begin < 0 || layer_begin + layer_count > c->num_layers)
+        return fail(DS_ERR_INVALID_ARG, "%s: layer range outside the pool", W);
+      if (h0s[e] < 0 || h0s[e] + head_count > c->num_heads)
+        return fail(DS_ERR_INVALID_ARG, "%s: head slice outside n_loc", W);
+    }
+    if (num_blocks > 0 && !block_ids) return fail(DS_ERR_INVALID_ARG, "%s: NULL block_ids", W);
+  }
+  const int64_t rows = (int64_t)layer_count * 2 * num_blocks;
+  if (rows == 0 || head_count == 0) return DS_OK;
+  const int64_t row_bytes = (int64_t)head_count * 16 * cache->head_dim * 2;
+  const int64_t crows = chunk_rows_for(row_bytes, rows);
+  const size_t need = ds_kv_migrate_staging_bytes(cache, role, layer_count, num_blocks, head_count);
+  if (!staging || staging_bytes < need)
+    return fail(DS_ERR_INVALID_ARG, "%s: staging must be >= %zu bytes", W, need);
+  cudaStream_t A = static_cast<cudaStream_t>(stream), B = comm->side;
+  char *stg = static_cast<char *>(staging);
+  const int64_t slot_bytes = crows * row_bytes;
+  const int64_t nchunks = (rows + crows - 1) / crows;
+  const bool send_side = role != DS_MIGRATE_RECV;
+  const ds_kv_cache *src = cache;
+  const ds_kv_cache *dst = role == DS_MIGRATE_SELF ? dst_cache : cache;
+  const int32_t *dst_ids = role == DS_MIGRATE_SELF ? dst_block_ids : block_ids;
+  const int32_t dst_h0 = role == DS_MIGRATE_SELF ? dst_head_begin : head_begin;
+  char *recv_base = role == DS_MIGRATE_SELF ? stg + 2 * slot_bytes : stg;
+
+  DS_CUDA(cudaEventRecord(comm->ev_start, A), W);
+  DS_CUDA(cudaStreamWaitEvent(B, comm->ev_start, 0), W);
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int slot = (int)(k & 1);
+    const int64_t r0 = k * crows, r1 = r0 + crows < rows ? r0 + crows : rows;
+    const size_t bytes = (size_t)((r1 - r0) * row_bytes);
+    char *sbuf = stg + slot * slot_bytes;
+    char *rbuf = recv_base + slot * slot_bytes;
+    if (send_side) {
+      // slot is free once the transfer of chunk k-2 has completed
+      if (k >= 2) DS_CUDA(cudaStreamWaitEvent(A, comm->ev_b[slot], 0), W);
+      if (ds_status s = kv_copy_checked(src, layer_begin, layer_count, block_ids, num_blocks,
+                                        head_begin, head_count, sbuf, slot_bytes, r0, r1, true, A, W))
+        return s;
+      DS_CUDA(cudaEventRecord(comm->ev_a[slot], A), W);
+      DS_CUDA(cudaStreamWaitEvent(B, comm->ev_a[slot], 0), W);  // packed (and, SELF: k-2 unpacked)
+    } else if (k >= 2) {
+      DS_CUDA(cudaStreamWaitEvent(B, comm->ev_a[slot], 0), W);  // unpack of chunk k-2 done
+    }
+    DS_NCCL(ncclGroupStart(), W);
+    if (role != DS_MIGRATE_RECV) DS_NCCL(ncclSend(sbuf, bytes, ncclUint8, peer, comm->comm, B), W);
+    if (role != DS_MIGRATE_SEND) DS_NCCL(ncclRecv(rbuf, bytes, ncclUint8, peer, comm->comm, B), W);
+    DS_NCCL(ncclGroupEnd(), W);
+    DS_CUDA(cudaEventRecord(comm->ev_b[slot], B), W);
+    if (role != DS_MIGRATE_SEND) {
+      DS_CUDA(cudaStreamWaitEvent(A, comm->ev_b[slot], 0), W);
+      // staging row r0 of the chunk sits at the start of the receive slot
+      if (ds_status s = kv_copy_checked(dst, layer_begin, layer_count, dst_ids, num_blocks,
+                                        dst_h0, head_count, rbuf, slot_bytes, r0, r1, false, A, W))
+        return s;
+      if (role == DS_MIGRATE_RECV) DS_CUDA(cudaEventRecord(comm->ev_a[slot], A), W);
+    }
+  }
+  // the caller's stream is ordered after every transfer of this call
+  DS_CUDA(cudaEventRecord(comm->ev_start, B), W);
+  DS_CUDA(cudaStreamWaitEvent(A, comm->ev_start, 0), W);
+  return DS_OK;
+}

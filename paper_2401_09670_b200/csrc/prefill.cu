@@ -1,0 +1,306 @@
+// prefill.cu — a2 + a3: causal prefill attention of one layer with the paged
+// K/V write fused in (tcgen05 / TMEM / TMA, sm_100a).
+//
+// What it computes (§2.1; App. A "attention only
+// operates among the tokens in the same request"; readings R1 scale, R2 causal):
+//   out[i] = sum_{j<=i} softmax_j(scale * q[i].k[j]) v[j]     per (sequence, head)
+//   cache[layer][K|V][bt[r][t/16]][h][t%16] = k|v[t][h]       (a3)
+//
+// B200 design (one CTA per (head, sequence, 128-row q tile), heaviest tiles first):
+//   warp 4  : TMA producer — Q tile once, then K_j / V_j tiles (j = 0..i, causal)
+//             into a 2-stage ring; after the loop it writes the diagonal K/V tile
+//             (the only one this CTA owns) into the paged cache with TMA tensor
+//             stores, one 16-token page per store (a3 fused: no extra HBM read).
+//   warp 5  : MMA issuer (one elected lane) — S_j = Q K_j^T into a double-buffered
+//             TMEM S (128x128 fp32), then O += P_{j-1} V_{j-1} into TMEM O; commits
+//             to mbarriers.
+//   warps 0-3: softmax / correction / epilogue — thread t owns row t (TMEM lane t):
+//             tcgen05.ld S row, online softmax in base 2 (scale*log2 e folded),
+//             lazy warp-uniform O rescale in TMEM, P (bf16, 128B-swizzled) to smem,
+//             final O / l -> bf16 -> global.
+// The S MMA of tile j+1 overlaps the softmax of tile j; the P.V MMA of tile j
+// overlaps the softmax of tile j+1.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ds {
+namespace {
+
+constexpr int kBM = 128, kBN = 128;
+constexpr int kThreads = 192;
+constexpr uint32_t kChunkBytes = 128 * 128;  // 128 rows x 128 B (64 bf16) swizzle atom column
+
+template <int D>
+struct Smem {
+  static constexpr uint32_t kTile = kBM * D * 2;  // one Q/K/V tile
+  static constexpr uint32_t Q = 0;
+  static constexpr uint32_t K0 = Q + kTile;
+  static constexpr uint32_t V0 = K0 + 2 * kTile;
+  static constexpr uint32_t P = V0 + 2 * kTile;
+  static constexpr uint32_t BAR = P + kBM * kBN * 2;
+  static constexpr uint32_t kBars = 12;
+  static constexpr uint32_t TMEM_SLOT = BAR + kBars * 8;
+  static constexpr uint32_t TOTAL = TMEM_SLOT + 16;
+  static constexpr uint32_t ALLOC = TOTAL + 1024;  // slack for 1024-B alignment
+};
+
+// barrier indices
+enum { B_Q = 0, B_K0, B_K1, B_V0, B_V1, B_E0, B_E1, B_S0, B_S1, B_P, B_O };
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                   const __grid_constant__ CUtensorMap tm_v,
+                   const __grid_constant__ CUtensorMap tm_cache, const PrefillArgs a) {
+  using S = Smem<D>;
+  constexpr int kChunks = D / 64;
+  const int h = blockIdx.x, r = blockIdx.y;
+  const int i = a.num_q_tiles - 1 - (int)blockIdx.z;  // heaviest (longest causal row) first
+  const int seq_start = a.cu_seqlens[r];
+  const int len = a.cu_seqlens[r + 1] - seq_start;
+  if (i * kBM >= len) return;
+  const int ntiles = i + 1;
+
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t *smem = smem_raw + (((raw + 1023u) & ~1023u) - raw);
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S::BAR);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + S::TMEM_SLOT);
+  const int warp = threadIdx.x >> 5;
+
+  if (threadIdx.x == 0) {
+    for (int b = B_Q; b <= B_O; ++b) mbar_init(&bars[b], b == B_P ? 128 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) {
+    tmem_alloc<512>(tmem_slot);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tO = tmem + 256;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ producer
+    if (elect_one()) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      tma_prefetch_desc(&tm_cache);
+      const int q_row0 = seq_start + i * kBM;
+      mbar_arrive_expect_tx(&bars[B_Q], S::kTile);
+#pragma unroll
+      for (int c = 0; c < kChunks; ++c)
+        tma_load_3d(smem + S::Q + c * kChunkBytes, &tm_q, &bars[B_Q], c * 64, h, q_row0);
+      for (int j = 0; j < ntiles; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(&bars[B_E0 + st], ((j >> 1) - 1) & 1);
+        const int kv_row0 = seq_start + j * kBN;
+        mbar_arrive_expect_tx(&bars[B_K0 + st], S::kTile);
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c)
+          tma_load_3d(smem + S::K0 + st * S::kTile + c * kChunkBytes, &tm_k, &bars[B_K0 + st],
+                      c * 64, h, kv_row0);
+        mbar_arrive_expect_tx(&bars[B_V0 + st], S::kTile);
+#pragma unroll
+        for (int c = 0; c < kChunks; ++c)
+          tma_load_3d(smem + S::V0 + st * S::kTile + c * kChunkBytes, &tm_v, &bars[B_V0 + st],
+                      c * 64, h, kv_row0);
+      }
+      // a3: the diagonal K/V tile (j == i) -> paged cache, one 16-token page per store.
+      const int st = i & 1;
+      mbar_wait(&bars[B_K0 + st], (i >> 1) & 1);
+      mbar_wait(&bars[B_V0 + st], (i >> 1) & 1);
+      const int rem = len - i * kBM;
+      const int npg = min(8, (rem + 15) >> 4);
+      const int32_t *bt = a.block_table + (size_t)r * a.max_blocks + i * 8;
+      for (int p = 0; p < npg; ++p) {
+        const int blk = bt[p];
+#pragma unroll
+        for (int kv = 0; kv < 2; ++kv) {
+          const uint8_t *tile = smem + (kv ? S::V0 : S::K0) + st * S::kTile;
+#pragma unroll
+          for (int c = 0; c < kChunks; ++c)
+            tma_store_4d(&tm_cache, tile + c * kChunkBytes + p * 16 * 128, c * 64, 0, h,
+                         (a.layer * 2 + kv) * a.num_blocks + blk);
+        }
+      }
+      bulk_commit_group();
+      bulk_wait_group_read0();
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, D, 0, 1);
+      mbar_wait(&bars[B_Q], 0);
+      tc_fence_after();
+      for (int j = 0; j <= ntiles; ++j) {
+        if (j < ntiles) {
+          const int st = j & 1;
+          mbar_wait(&bars[B_K0 + st], (j >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * kChunkBytes + (kk & 3) * 32;
+            const uint64_t da = smem_desc_sw128(sbase + S::Q + off, 16, 1024);
+            const uint64_t db = smem_desc_sw128(sbase + S::K0 + st * S::kTile + off, 16, 1024);
+            umma_ss(tmem + st * kBN, da, db, idesc_s, kk > 0);
+          }
+          umma_commit(&bars[B_S0 + st]);
+        }
+        if (j >= 1) {
+          const int jj = j - 1, st = jj & 1;
+          mbar_wait(&bars[B_P], jj & 1);
+          mbar_wait(&bars[B_V0 + st], (jj >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kBN / 16; ++kk) {
+            const uint64_t da =
+                smem_desc_sw128(sbase + S::P + (kk >> 2) * kChunkBytes + (kk & 3) * 32, 16, 1024);
+            const uint64_t db =
+                smem_desc_sw128(sbase + S::V0 + st * S::kTile + kk * 16 * 128, kChunkBytes, 1024);
+            umma_ss(tO, da, db, idesc_o, (jj > 0 || kk > 0));
+          }
+          umma_commit(&bars[B_O]);
+          umma_commit(&bars[B_E0 + st]);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ softmax warps 0-3
+    const int row = threadIdx.x;  // TMEM lane == q row within the tile
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const float sl2 = a.scale_log2;
+    float m = -__int_as_float(0x7f800000), l = 0.f;
+    uint8_t *prow = smem + S::P + row * 128;
+    for (int j = 0; j < ntiles; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&bars[B_S0 + sb], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t sr[4][32];
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) tmem_ld32(tmem + lane_off + sb * kBN + cc * 32, sr[cc]);
+      tmem_wait_ld();
+      const bool diag = (j == i);
+      float mx = -__int_as_float(0x7f800000);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          float x = __uint_as_float(sr[cc][e]) * sl2;
+          if (diag && (cc * 32 + e) > row) x = -__int_as_float(0x7f800000);
+          sr[cc][e] = __float_as_uint(x);
+          mx = fmaxf(mx, x);
+        }
+      const float m_new = fmaxf(m, mx);
+      const float alpha = ex2(m - m_new);
+      float rs = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float p = ex2(__uint_as_float(sr[cc][e]) - m_new);
+          rs += p;
+          sr[cc][e] = __float_as_uint(p);
+        }
+      l = l * alpha + rs;
+      m = m_new;
+      if (j > 0) {
+        // P smem and O are in use by P_{j-1} V_{j-1}: wait for it
+        mbar_wait(&bars[B_O], (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha < 1.f)) {
+#pragma unroll
+          for (int cc = 0; cc < D / 32; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(tO + lane_off + cc * 32, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st32(tO + lane_off + cc * 32, o);
+          }
+          tmem_wait_st();
+        }
+      }
+      // P row -> smem, K-major SWIZZLE_128B: 16-B piece pc of chunk c2 at pc ^ (row & 7)
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2)
+#pragma unroll
+        for (int pc = 0; pc < 8; ++pc) {
+          const int cc = c2 * 2 + (pc >> 2), e0 = (pc & 3) * 8;
+          uint4 v;
+          v.x = pack_bf16(__uint_as_float(sr[cc][e0 + 0]), __uint_as_float(sr[cc][e0 + 1]));
+          v.y = pack_bf16(__uint_as_float(sr[cc][e0 + 2]), __uint_as_float(sr[cc][e0 + 3]));
+          v.z = pack_bf16(__uint_as_float(sr[cc][e0 + 4]), __uint_as_float(sr[cc][e0 + 5]));
+          v.w = pack_bf16(__uint_as_float(sr[cc][e0 + 6]), __uint_as_float(sr[cc][e0 + 7]));
+          *reinterpret_cast<uint4 *>(prow + c2 * kChunkBytes + ((pc ^ (row & 7)) << 4)) = v;
+        }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(&bars[B_P]);
+    }
+    // epilogue: O / l -> bf16 -> global (rows inside the sequence only)
+    mbar_wait(&bars[B_O], (ntiles - 1) & 1);
+    tc_fence_after();
+    const float inv_l = 1.f / l;
+    const int q_pos = i * kBM + row;
+    uint16_t *orow = reinterpret_cast<uint16_t *>(a.out) +
+                     ((size_t)(seq_start + q_pos) * a.n_loc + h) * D;
+#pragma unroll
+    for (int cc = 0; cc < D / 32; ++cc) {
+      uint32_t o[32];
+      tmem_ld32(tO + lane_off + cc * 32, o);
+      tmem_wait_ld();
+      if (q_pos < len) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint4 v;
+          v.x = pack_bf16(__uint_as_float(o[u * 8 + 0]) * inv_l, __uint_as_float(o[u * 8 + 1]) * inv_l);
+          v.y = pack_bf16(__uint_as_float(o[u * 8 + 2]) * inv_l, __uint_as_float(o[u * 8 + 3]) * inv_l);
+          v.z = pack_bf16(__uint_as_float(o[u * 8 + 4]) * inv_l, __uint_as_float(o[u * 8 + 5]) * inv_l);
+          v.w = pack_bf16(__uint_as_float(o[u * 8 + 6]) * inv_l, __uint_as_float(o[u * 8 + 7]) * inv_l);
+          *reinterpret_cast<uint4 *>(orow + cc * 32 + u * 8) = v;
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+}  // namespace
+
+size_t prefill_smem_bytes(int head_dim) {
+  return head_dim == 128 ? Smem<128>::ALLOC : Smem<64>::ALLOC;
+}
+
+cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
+                           const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
+                           cudaStream_t stream) {
+  dim3 grid(a.n_loc, a.num_seqs, a.num_q_tiles);
+  const size_t smem = prefill_smem_bytes(head_dim);
+  cudaError_t e;
+  if (head_dim == 128) {
+    e = cudaFuncSetAttribute(prefill_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    prefill_kernel<128><<<grid, kThreads, smem, stream>>>(tm_q, tm_k, tm_v, tm_cache, a);
+  } else {
+    e = cudaFuncSetAttribute(prefill_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    prefill_kernel<64><<<grid, kThreads, smem, stream>>>(tm_q, tm_k, tm_v, tm_cache, a);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ds

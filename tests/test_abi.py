@@ -1,0 +1,183 @@
+"""C-ABI boundary tests that run without a GPU (-m "not gpu").
+
+* libds.so loads and exports every entry point include/ds.h declares;
+* a1 (ds_block_table, host code) is bit-exact against the oracle allocator on
+  randomised APPEND/FREE traces, including exhaustion (all-or-nothing);
+* argument validation rejects bad calls with DS_ERR_INVALID_ARG before touching
+  the device, and a well-formed compute call on a GPU-less host fails loudly
+  with DS_ERR_CUDA (no CPU fallback).
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2401_09670_b200 as ds
+import synthetic as syn
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    txt = open(os.path.join(ROOT, "include", "ds.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(ds_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_header_symbols_exported():
+    declared = _declared_symbols()
+    assert len(declared) >= 17
+    lib = ctypes.CDLL(ds.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(ds.EXPORTED) == declared
+
+
+def test_build_info_reports_nccl():
+    info = ds.ds_build_info()
+    assert info.startswith("libds sm_100a nccl 2.")
+
+
+def _rand_trace(seed, nseq=6, steps=60):
+    g = syn.rng(seed)
+    ops = []
+    lens = np.zeros(nseq, dtype=np.int32)
+    live = np.zeros(nseq, dtype=bool)
+    for _ in range(steps):
+        s = int(g.integers(nseq))
+        r = g.random()
+        if live[s] and r < 0.2:
+            ops.append(("free", s, int(lens[s])))
+            lens[s] = 0
+            live[s] = False
+        else:
+            add = int(g.integers(1, 40)) if r < 0.6 else 1
+            ops.append(("append", s, int(lens[s]), add))
+            lens[s] += add
+            live[s] = True
+    return ops
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_block_table_bit_exact_vs_oracle(oracle_mod, seed):
+    nseq, nb, maxb = 6, 40, 16
+    pool = ds.Pool(nb)
+    opool = oracle_mod.Pool(1, nb, 1, 64)
+    t_ds = np.full((nseq, maxb), -1, dtype=np.int32)
+    t_or = t_ds.copy()
+    for op in _rand_trace(seed, nseq):
+        if op[0] == "append":
+            _, s, cur, add = op
+            row_ds, row_or = t_ds[s:s + 1].copy(), t_or[s:s + 1].copy()
+            try:
+                ds.ds_block_table(pool, ds.DS_BT_APPEND, [cur], [add], row_ds)
+                rc_ds = 0
+            except ds.DSError as e:
+                rc_ds = e.status
+            rc_or = opool.append([cur], [add], row_or)
+            assert rc_ds == rc_or
+            t_ds[s], t_or[s] = row_ds[0], row_or[0]
+            if rc_ds != 0:
+                # undo the host-side length bookkeeping of this trace step: sequence is reset
+                row = t_ds[s:s + 1].copy()
+                ds.ds_block_table(pool, ds.DS_BT_FREE, [cur], None, row)
+                opool.free([cur], t_or[s:s + 1].copy()) if cur else None
+                t_or[s:s + 1] = -1
+                t_ds[s:s + 1] = -1
+        else:
+            _, s, cur = op
+            row_ds, row_or = t_ds[s:s + 1].copy(), t_or[s:s + 1].copy()
+            ds.ds_block_table(pool, ds.DS_BT_FREE, [cur], None, row_ds)
+            assert opool.free([cur], row_or) == 0
+            t_ds[s], t_or[s] = row_ds[0], row_or[0]
+        assert np.array_equal(t_ds, t_or)
+        assert pool.num_free == opool.num_free
+
+
+def test_block_table_batch_and_exhaustion(oracle_mod):
+    lens = [33, 1, 16, 17, 200]
+    pool, opool = ds.Pool(21), oracle_mod.Pool(1, 21, 1, 64)
+    t1, t2 = np.full((5, 16), -1, np.int32), np.full((5, 16), -1, np.int32)
+    nf = ds.ds_block_table(pool, ds.DS_BT_APPEND, [0] * 5, lens, t1)
+    assert opool.append([0] * 5, lens, t2) == 0
+    assert np.array_equal(t1, t2) and nf == opool.num_free == 21 - 20
+    t3 = np.full((1, 16), -1, np.int32)
+    with pytest.raises(ds.DSError) as ei:
+        ds.ds_block_table(pool, ds.DS_BT_APPEND, [0], [33], t3)
+    assert ei.value.status == ds.DS_ERR_NO_BLOCKS
+    assert np.all(t3 == -1) and pool.num_free == 1
+
+
+def test_block_table_rejects_bad_args():
+    pool = ds.Pool(8)
+    t = np.full((1, 2), -1, np.int32)
+    for args in ((ds.DS_BT_APPEND, [-1], [1]), (ds.DS_BT_APPEND, [0], [33]), (7, [0], [1])):
+        with pytest.raises(ds.DSError) as ei:
+            ds.ds_block_table(pool, args[0], args[1], args[2], t)
+        assert ei.value.status == ds.DS_ERR_INVALID_ARG
+    with pytest.raises(ds.DSError):  # FREE of never-allocated ids
+        ds.ds_block_table(pool, ds.DS_BT_FREE, [16], None, np.array([[3, -1]], np.int32))
+    assert pool.num_free == 8
+
+
+def _cache(base=0x10000, L=2, NB=64, n=4, D=64):
+    return ds.ds_kv_cache(base, L, NB, n, 16, D)
+
+
+FAKE = 0x7F0000000000  # aligned non-null address; never dereferenced on a GPU-less host
+
+
+def test_prefill_validation_then_no_device():
+    lib = ds.lib()
+    c = _cache()
+    args = lambda **kw: dict(dict(q=FAKE, k=FAKE, v=FAKE, out=FAKE, cu=FAKE, B=2, T=40, maxl=33,
+                                  layer=1, bt=FAKE, maxb=4, scale=0.125), **kw)
+    def call(a, cache=c):
+        return lib.ds_prefill_attn(a["q"], a["k"], a["v"], a["out"], a["cu"], a["B"], a["T"], a["maxl"],
+                                   ctypes.byref(cache), a["layer"], a["bt"], a["maxb"], a["scale"], None)
+    assert call(args(q=FAKE + 2)) == ds.DS_ERR_INVALID_ARG
+    assert call(args(layer=2)) == ds.DS_ERR_INVALID_ARG
+    assert call(args(maxb=2)) == ds.DS_ERR_INVALID_ARG
+    assert call(args(scale=0.0)) == ds.DS_ERR_INVALID_ARG
+    assert call(args(), cache=_cache(D=96)) == ds.DS_ERR_INVALID_ARG
+    assert call(args(B=0)) == ds.DS_OK  # empty batch is a no-op
+    rc = call(args())
+    assert rc == ds.DS_ERR_CUDA, ds.ds_last_error()
+    assert "ds_prefill_attn" in ds.ds_last_error()
+
+
+def test_decode_validation_and_workspace():
+    lib = ds.lib()
+    c = _cache(n=4, D=128)
+    assert ds.ds_decode_workspace_bytes(1, 4, 128, 543) >= 4 * (128 + 2) * 4
+    ws = ds.ds_decode_workspace_bytes(1, 4, 128, 543)
+    call = lambda maxc, ws_ptr, ws_bytes: lib.ds_decode_attn(FAKE, FAKE, FAKE, FAKE, ctypes.byref(c), 0, FAKE, 40,
+                                                           FAKE, 1, maxc, 0.088, ws_ptr, ws_bytes, None)
+    assert call(543, None, 0) == ds.DS_ERR_INVALID_ARG  # needs split workspace
+    assert call(640, FAKE, ws) == ds.DS_ERR_INVALID_ARG  # 640/16 >= 40 pages
+    assert call(543, FAKE, ws) == ds.DS_ERR_CUDA
+
+
+def test_staging_sizes():
+    c = _cache(L=40, NB=1000, n=40, D=128)
+    assert ds.lib().ds_kv_staging_bytes(ctypes.byref(c), 40, 32, 40) == 40 * 2 * 32 * 40 * 4096
+    # per request of OPT-13B at 512 tokens: 419,430,400 bytes
+    assert ds.lib().ds_kv_staging_bytes(ctypes.byref(c), 40, 32, 40) == 419_430_400
+    row = 40 * 4096
+    mig = ds.lib().ds_kv_migrate_staging_bytes(ctypes.byref(c), ds.DS_MIGRATE_SEND, 40, 32, 40)
+    assert mig == 2 * ((64 << 20) // row) * row
+    mig_self = ds.lib().ds_kv_migrate_staging_bytes(ctypes.byref(c), ds.DS_MIGRATE_SELF, 40, 32, 40)
+    assert mig_self == 2 * mig
+    small = ds.lib().ds_kv_migrate_staging_bytes(ctypes.byref(c), ds.DS_MIGRATE_SEND, 1, 1, 40)
+    assert small == 2 * 2 * row  # chunk clamps to the 2 rows that exist
+
+
+def test_pack_validation():
+    lib = ds.lib()
+    c = _cache(L=2, NB=16, n=4, D=64)
+    assert lib.ds_kv_pack(ctypes.byref(c), 1, 2, FAKE, 3, 0, 4, FAKE, 1 << 20, None) == ds.DS_ERR_INVALID_ARG
+    assert lib.ds_kv_pack(ctypes.byref(c), 0, 2, FAKE, 3, 2, 3, FAKE, 1 << 20, None) == ds.DS_ERR_INVALID_ARG
+    assert lib.ds_kv_pack(ctypes.byref(c), 0, 2, FAKE, 3, 0, 4, FAKE, 100, None) == ds.DS_ERR_INVALID_ARG
+    assert lib.ds_kv_pack(ctypes.byref(c), 0, 2, FAKE, 3, 0, 4, FAKE, 1 << 20, None) == ds.DS_ERR_CUDA

@@ -1,0 +1,328 @@
+"""GPU parity: the CUDA path through the C ABI vs the fp64 CPU oracle (-m gpu).
+
+Bars (BASELINE.json north_star): block tables and migrated / paged bytes
+bit-exact; attention outputs within 2e-2 max relative error per (token, head)
+vector (oracle.max_rel_err). The expected error is ~2^-9 (bf16 P and bf16 out);
+anything above 5e-3 on N(0,1) inputs is treated as a bug signal (checked too).
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2401_09670_b200 as ds  # noqa: E402
+import synthetic as syn  # noqa: E402
+from tests.gpu_util import i32, pages_match, to_bits, to_dev, to_f64  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+WARN = 5e-3
+BS = 16
+
+
+def _ceil(a, b):
+    return -(-a // b)
+
+
+class Side:
+    """One pool (GPU + oracle mirror) with identical block tables."""
+
+    def __init__(self, oracle_mod, layers, num_blocks, heads, head_dim):
+        self.cache = ds.KVCache.empty(layers, num_blocks, heads, head_dim)
+        self.cache.tensor.zero_()
+        self.pool = ds.Pool(num_blocks)
+        self.opool = oracle_mod.Pool(layers, num_blocks, heads, head_dim)
+
+    def append(self, cur, add, table_ds, table_or):
+        ds.ds_block_table(self.pool, ds.DS_BT_APPEND, cur, add, table_ds)
+        assert self.opool.append(cur, add, table_or) == 0
+        assert np.array_equal(table_ds, table_or)
+
+    def fragment(self, seed, n_rows):
+        """allocate n_rows single-page rows and free a random half of them"""
+        junk = np.full((n_rows, 1), -1, np.int32)
+        junk_o = junk.copy()
+        self.append([0] * n_rows, [16] * n_rows, junk, junk_o)
+        sel = np.sort(syn.rng(seed).permutation(n_rows)[: n_rows // 2])
+        r1, r2 = np.ascontiguousarray(junk[sel]), np.ascontiguousarray(junk_o[sel])
+        ds.ds_block_table(self.pool, ds.DS_BT_FREE, [16] * len(sel), None, r1)
+        assert self.opool.free([16] * len(sel), r2) == 0
+
+
+def run_prefill(oracle_mod, lens, n, d, seed=0, layers=1, layer=0, q_sigma=1.0, fragment=0,
+                full_check=True, sample_rows=None):
+    b = syn.prefill_batch(seed, lens, n, d, q_sigma=q_sigma)
+    maxb = _ceil(max(lens), BS)
+    nblocks = sum(_ceil(l, BS) for l in lens) + fragment + 4
+    side = Side(oracle_mod, layers, nblocks, n, d)
+    if fragment:
+        side.fragment(seed + 1, fragment)
+    t_ds = np.full((len(lens), maxb), -1, np.int32)
+    t_or = t_ds.copy()
+    side.append([0] * len(lens), lens, t_ds, t_or)
+    q, k, v = to_dev(b.q), to_dev(b.k), to_dev(b.v)
+    out = torch.full_like(q, float("nan"))
+    scale = 1.0 / math.sqrt(d)
+    ds.ds_prefill_attn(q, k, v, out, i32(b.cu_seqlens), int(max(lens)), side.cache, layer, i32(t_ds), scale)
+    torch.cuda.synchronize()
+    got = to_f64(out)
+    if full_check:
+        ref = oracle_mod.prefill(b.q, b.k, b.v, b.cu_seqlens, scale)
+        err = oracle_mod.max_rel_err(got, ref)
+    else:
+        err = 0.0
+        for (r, i, h) in sample_rows:
+            ref = oracle_mod.prefill_row(b.q, b.k, b.v, b.cu_seqlens, r, i, h, scale)
+            err = max(err, oracle_mod.max_rel_err(got[b.cu_seqlens[r] + i, h], ref))
+    side.opool.write_prefill(layer, b.k, b.v, b.cu_seqlens, t_or)
+    return b, side, t_ds, got, err
+
+
+# ------------------------------------------------------------------ a2 + a3
+@pytest.mark.parametrize("lens,n,d", [
+    ([32], 4, 64),                       # config 1 prompt
+    ([1], 1, 64), ([15, 16, 17], 2, 64), ([127, 128, 129], 4, 128),
+    ([511, 1, 300, 64], 4, 128), ([2048], 1, 128), ([1000, 257], 2, 64),
+])
+def test_prefill_parity_and_paged_write(oracle_mod, lens, n, d):
+    b, side, table, got, err = run_prefill(oracle_mod, lens, n, d, seed=len(lens) + n + d, layers=2,
+                                           layer=1, fragment=6)
+    assert not np.isnan(got).any()
+    assert err <= TOL and err <= WARN, err
+    cache_bits = to_bits(side.cache.tensor)
+    assert pages_match(cache_bits, side.opool, 1, lens, table)
+
+
+def test_prefill_stress_large_logits(oracle_mod):
+    # q x 8: logits of O(100) exercise the online-softmax rescaling
+    _, _, _, got, err = run_prefill(oracle_mod, [300, 77], 2, 128, seed=5, q_sigma=8.0)
+    assert err <= TOL, err
+
+
+def test_prefill_many_heads_ragged(oracle_mod):
+    _, side, table, got, err = run_prefill(oracle_mod, [130, 45, 260], 40, 128, seed=9)
+    assert err <= TOL and err <= WARN, err
+
+
+def test_prefill_full_size_config2_sampled(oracle_mod):
+    # OPT-13B geometry, 16 x 512-token prompts (8192 tokens): the bench's launch
+    g = syn.rng(3)
+    lens = [512] * 16
+    rows = [(int(g.integers(16)), int(i), int(g.integers(40))) for i in
+            list(g.integers(0, 512, 40)) + [0, 127, 128, 255, 511]]
+    _, side, table, got, err = run_prefill(oracle_mod, lens, 40, 128, seed=11, full_check=False,
+                                           sample_rows=rows)
+    assert err <= TOL and err <= WARN, err
+    assert not np.isnan(got).any()
+
+
+# ------------------------------------------------------------------ a7 + a8
+def run_decode(oracle_mod, ctx, n, d, seed=0, steps=1, fragment=0, q_sigma=1.0, max_cache_len=None):
+    """Prefill (GPU) the first ctx tokens of each sequence, then `steps` decode
+    steps; compare each step with the oracle's decode."""
+    B = len(ctx)
+    hist = [max(c, 1) for c in ctx]
+    total = [c + steps for c in ctx]
+    maxb = _ceil(max(total) + 1, BS)
+    nblocks = sum(_ceil(t + 1, BS) for t in total) + fragment + 4
+    side = Side(oracle_mod, 1, nblocks, n, d)
+    if fragment:
+        side.fragment(seed + 7, fragment)
+    t_ds = np.full((B, maxb), -1, np.int32)
+    t_or = t_ds.copy()
+    side.append([0] * B, ctx, t_ds, t_or)
+    b = syn.prefill_batch(seed, hist, n, d)
+    if any(c > 0 for c in ctx):
+        # sequences with c == 0 still get a 1-token prefill input but no pages; feed only c>0 ones
+        idx = [i for i, c in enumerate(ctx) if c > 0]
+        sel = np.concatenate([np.arange(b.cu_seqlens[i], b.cu_seqlens[i] + ctx[i]) for i in idx])
+        lens = [ctx[i] for i in idx]
+        cu = syn.cu_seqlens(lens)
+        tsub = np.ascontiguousarray(t_ds[idx])
+        qh, kh, vh = b.q[sel], b.k[sel], b.v[sel]
+        out = torch.empty_like(to_dev(qh))
+        ds.ds_prefill_attn(to_dev(qh), to_dev(kh), to_dev(vh), out, i32(cu), max(lens), side.cache, 0,
+                           i32(tsub), 1.0 / math.sqrt(d))
+        side.opool.write_prefill(0, kh, vh, cu, np.ascontiguousarray(t_or[idx]))
+    cur = list(ctx)
+    errs = []
+    scale = 1.0 / math.sqrt(d)
+    for s in range(steps):
+        side.append(cur, [1] * B, t_ds, t_or)
+        db = syn.decode_batch(seed * 100 + s, B, n, d, q_sigma=q_sigma)
+        out = torch.full((B, n, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+        mcl = max(cur) if max_cache_len is None else max_cache_len
+        ws = torch.empty(max(ds.ds_decode_workspace_bytes(B, n, d, mcl), 16) // 4 + 4,
+                         dtype=torch.float32, device="cuda")
+        ds.ds_decode_attn(to_dev(db.q), to_dev(db.k_new), to_dev(db.v_new), out, side.cache, 0, i32(t_ds),
+                          i32(cur), mcl, scale, ws)
+        torch.cuda.synchronize()
+        ref = side.opool.decode(0, db.q, db.k_new, db.v_new, t_or, cur, scale)
+        errs.append(oracle_mod.max_rel_err(to_f64(out), ref))
+        cur = [c + 1 for c in cur]
+    return side, t_ds, cur, errs
+
+
+def test_config1_prompt32_plus_8_decode_steps(oracle_mod):
+    """BASELINE config 1: L=1, 4 heads x 64, prompt 32 + 8 decode steps, block 16
+    (page 3 is allocated at the first decode step, position 32)."""
+    side, table, cur, errs = run_decode(oracle_mod, [32], 4, 64, seed=1, steps=8)
+    assert max(errs) <= TOL and max(errs) <= WARN, errs
+    assert int((table[0] >= 0).sum()) == 3
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
+
+
+@pytest.mark.parametrize("ctx,n,d", [
+    ([0], 1, 64), ([15, 16, 17, 31, 32, 1], 2, 64), ([543], 40, 128), ([100, 2000, 7], 4, 128),
+    ([int(x) for x in syn.rng(4).integers(0, 700, 64)], 8, 128),
+])
+def test_decode_parity(oracle_mod, ctx, n, d):
+    side, table, cur, errs = run_decode(oracle_mod, ctx, n, d, seed=sum(ctx) % 97, steps=2, fragment=5)
+    assert max(errs) <= TOL and max(errs) <= WARN, errs
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
+
+
+def test_decode_split_invariance(oracle_mod):
+    # the same step planned with a larger max_cache_len uses a different split-K plan
+    for mcl in (None, 1500):
+        _, _, _, errs = run_decode(oracle_mod, [300, 5], 2, 128, seed=3, steps=1, max_cache_len=mcl)
+        assert max(errs) <= WARN, (mcl, errs)
+
+
+def test_decode_stress_large_logits(oracle_mod):
+    _, _, _, errs = run_decode(oracle_mod, [400, 33], 2, 128, seed=8, steps=1, q_sigma=8.0)
+    assert max(errs) <= TOL, errs
+
+
+def test_decode_batch256_config3_shape_sampled(oracle_mod):
+    ctx = [int(x) for x in syn.rng(12).integers(200, 900, 256)]
+    _, _, _, errs = run_decode(oracle_mod, ctx, 8, 128, seed=12, steps=1)
+    assert max(errs) <= WARN, errs
+
+
+# ------------------------------------------------------------------ a4 - a6
+def test_pack_unpack_loopback_bit_exact(oracle_mod):
+    lens = [40, 17, 100]
+    n, d, L = 8, 128, 3
+    b = syn.prefill_batch(21, lens, n, d)
+    src = Side(oracle_mod, L, 32, n, d)
+    dst = Side(oracle_mod, L, 48, 4, d)  # decode rank holds heads 4..7 (TP slice)
+    dst.fragment(3, 9)
+    tp, tpo = np.full((3, 8), -1, np.int32), np.full((3, 8), -1, np.int32)
+    td, tdo = np.full((3, 8), -1, np.int32), np.full((3, 8), -1, np.int32)
+    src.append([0] * 3, lens, tp, tpo)
+    dst.append([0] * 3, lens, td, tdo)
+    out = torch.empty((sum(lens), n, d), dtype=torch.bfloat16, device="cuda")
+    for layer in range(L):
+        ds.ds_prefill_attn(to_dev(b.q), to_dev(b.k), to_dev(b.v), out, i32(b.cu_seqlens), max(lens), src.cache,
+                           layer, i32(tp), 0.088)
+        src.opool.write_prefill(layer, b.k, b.v, b.cu_seqlens, tpo)
+    sblk = np.concatenate([tp[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+    dblk = np.concatenate([td[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+    nbytes = ds.ds_kv_staging_bytes(src.cache, 2, len(sblk), 4)
+    staging = torch.empty(nbytes // 2, dtype=torch.bfloat16, device="cuda")
+    ds.ds_kv_pack(src.cache, 1, 2, i32(sblk), 4, 4, staging)
+    ds.ds_kv_unpack(dst.cache, 1, 2, i32(dblk), 0, 4, staging)
+    torch.cuda.synchronize()
+    moved = oracle_mod.migrate(src.opool, dst.opool, 1, 2, sblk, dblk, 4, 0, 4)
+    assert moved == nbytes
+    bits = to_bits(dst.cache.tensor)
+    for layer in (1, 2):
+        assert pages_match(bits, dst.opool, layer, lens, td)
+    assert not bits[0].any()  # layer 0 untouched
+
+
+def test_migrate_self_through_nccl(oracle_mod):
+    """N=1 loopback through NCCL (send + recv to self in one group), several
+    chunks so the 2-slot ring wraps."""
+    lens = [600, 333]
+    n, d, L = 40, 128, 4
+    b = syn.prefill_batch(22, lens, n, d)
+    src = Side(oracle_mod, L, 80, n, d)
+    dst = Side(oracle_mod, L, 90, n, d)
+    dst.fragment(4, 10)
+    tp, tpo = np.full((2, 40), -1, np.int32), np.full((2, 40), -1, np.int32)
+    td, tdo = tp.copy(), tpo.copy()
+    src.append([0, 0], lens, tp, tpo)
+    dst.append([0, 0], lens, td, tdo)
+    out = torch.empty((sum(lens), n, d), dtype=torch.bfloat16, device="cuda")
+    for layer in range(L):
+        ds.ds_prefill_attn(to_dev(b.q), to_dev(b.k), to_dev(b.v), out, i32(b.cu_seqlens), max(lens), src.cache,
+                           layer, i32(tp), 0.088)
+        src.opool.write_prefill(layer, b.k, b.v, b.cu_seqlens, tpo)
+    sblk = np.concatenate([tp[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+    dblk = np.concatenate([td[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+    comm = ds.ds_comm_init(ds.ds_comm_get_unique_id(), 1, 0)
+    need = ds.ds_kv_migrate_staging_bytes(src.cache, ds.DS_MIGRATE_SELF, L, len(sblk), n)
+    staging = torch.empty(need, dtype=torch.uint8, device="cuda")
+    ds.ds_kv_migrate(comm, ds.DS_MIGRATE_SELF, 0, src.cache, 0, L, i32(sblk), 0, n, staging,
+                     dst_cache=dst.cache, dst_block_ids=i32(dblk), dst_head_begin=0)
+    torch.cuda.synchronize()
+    comm.close()
+    oracle_mod.migrate(src.opool, dst.opool, 0, L, sblk, dblk, 0, 0, n)
+    bits = to_bits(dst.cache.tensor)
+    for layer in range(L):
+        assert pages_match(bits, dst.opool, layer, lens, td)
+
+
+def test_end_to_end_prefill_migrate_decode(oracle_mod):
+    """The whole path for one small batch: prefill -> migrate (SELF) -> 3 decode
+    steps on the decode pool, compared with the oracle doing the same."""
+    lens = [70, 33, 16]
+    n, d, L = 4, 128, 2
+    B = len(lens)
+    b = syn.prefill_batch(31, lens, n, d)
+    P = Side(oracle_mod, L, 24, n, d)
+    D = Side(oracle_mod, L, 40, n, d)
+    D.fragment(2, 8)
+    tp, tpo = np.full((B, 8), -1, np.int32), np.full((B, 8), -1, np.int32)
+    td, tdo = tp.copy(), tpo.copy()
+    P.append([0] * B, lens, tp, tpo)
+    D.append([0] * B, lens, td, tdo)
+    out = torch.empty((sum(lens), n, d), dtype=torch.bfloat16, device="cuda")
+    scale = 1 / math.sqrt(d)
+    for layer in range(L):
+        ds.ds_prefill_attn(to_dev(b.q), to_dev(b.k), to_dev(b.v), out, i32(b.cu_seqlens), max(lens), P.cache,
+                           layer, i32(tp), scale)
+        P.opool.write_prefill(layer, b.k, b.v, b.cu_seqlens, tpo)
+    sblk = np.concatenate([tp[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+    dblk = np.concatenate([td[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+    comm = ds.ds_comm_init(ds.ds_comm_get_unique_id(), 1, 0)
+    staging = torch.empty(ds.ds_kv_migrate_staging_bytes(P.cache, ds.DS_MIGRATE_SELF, L, len(sblk), n),
+                          dtype=torch.uint8, device="cuda")
+    ds.ds_kv_migrate(comm, ds.DS_MIGRATE_SELF, 0, P.cache, 0, L, i32(sblk), 0, n, staging,
+                     dst_cache=D.cache, dst_block_ids=i32(dblk))
+    oracle_mod.migrate(P.opool, D.opool, 0, L, sblk, dblk, 0, 0, n)
+    # prefill side frees its pages after the pull
+    ds.ds_block_table(P.pool, ds.DS_BT_FREE, lens, None, tp)
+    assert P.opool.free(lens, tpo) == 0 and np.array_equal(tp, tpo)
+    cur = list(lens)
+    for s in range(3):
+        D.append(cur, [1] * B, td, tdo)
+        db = syn.decode_batch(500 + s, B, n, d)
+        for layer in range(L):
+            o = torch.empty((B, n, d), dtype=torch.bfloat16, device="cuda")
+            ws = torch.empty(ds.ds_decode_workspace_bytes(B, n, d, max(cur)) // 4 + 4, dtype=torch.float32,
+                             device="cuda")
+            ds.ds_decode_attn(to_dev(db.q), to_dev(db.k_new), to_dev(db.v_new), o, D.cache, layer, i32(td),
+                              i32(cur), max(cur), scale, ws)
+            torch.cuda.synchronize()
+            ref = D.opool.decode(layer, db.q, db.k_new, db.v_new, tdo, cur, scale)
+            assert oracle_mod.max_rel_err(to_f64(o), ref) <= WARN
+        cur = [c + 1 for c in cur]
+    comm.close()
+    bits = to_bits(D.cache.tensor)
+    for layer in range(L):
+        assert pages_match(bits, D.opool, layer, cur, td)
+
+
+def test_invalid_args_raise_before_launch():
+    c = ds.KVCache.empty(1, 4, 2, 64)
+    q = torch.zeros((3, 2, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ds.DSError) as ei:
+        ds.ds_prefill_attn(q, q, q, q, i32([0, 3]), 3, c, 1, i32([[0]]), 0.125)
+    assert ei.value.status == ds.DS_ERR_INVALID_ARG
