@@ -16,7 +16,7 @@ if not torch.cuda.is_available():
 
 import paper_2401_09670_b200 as ds  # noqa: E402
 import synthetic as syn  # noqa: E402
-from tests.gpu_util import i32, pages_match, to_bits, to_dev, to_f64  # noqa: E402
+from gpu_util import i32, pages_match, to_bits, to_dev, to_f64  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 TOL = 2e-2
