@@ -200,14 +200,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       const float m_new = fmaxf(m, mx);
       const float alpha = ex2(m - m_new);
+      // p = 2^(x - m) rounded to bf16 (the P operand of the P.V MMA); the row sum
+      // is taken over the same rounded values so numerator and normaliser agree.
+      uint32_t pk[64];
       float rs = 0.f;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc)
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float p = ex2(__uint_as_float(sr[cc][e]) - m_new);
-          rs += p;
-          sr[cc][e] = __float_as_uint(p);
+        for (int e = 0; e < 32; e += 2) {
+          const uint32_t pr = pack_bf16(ex2(__uint_as_float(sr[cc][e]) - m_new),
+                                        ex2(__uint_as_float(sr[cc][e + 1]) - m_new));
+          rs += bf16lo(pr) + bf16hi(pr);
+          pk[cc * 16 + e / 2] = pr;
         }
       l = l * alpha + rs;
       m = m_new;
@@ -233,12 +237,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c2 = 0; c2 < 2; ++c2)
 #pragma unroll
         for (int pc = 0; pc < 8; ++pc) {
-          const int cc = c2 * 2 + (pc >> 2), e0 = (pc & 3) * 8;
-          uint4 v;
-          v.x = pack_bf16(__uint_as_float(sr[cc][e0 + 0]), __uint_as_float(sr[cc][e0 + 1]));
-          v.y = pack_bf16(__uint_as_float(sr[cc][e0 + 2]), __uint_as_float(sr[cc][e0 + 3]));
-          v.z = pack_bf16(__uint_as_float(sr[cc][e0 + 4]), __uint_as_float(sr[cc][e0 + 5]));
-          v.w = pack_bf16(__uint_as_float(sr[cc][e0 + 6]), __uint_as_float(sr[cc][e0 + 7]));
+          const int w0 = c2 * 32 + pc * 4;
+          const uint4 v = make_uint4(pk[w0], pk[w0 + 1], pk[w0 + 2], pk[w0 + 3]);
           *reinterpret_cast<uint4 *>(prow + c2 * kChunkBytes + ((pc ^ (row & 7)) << 4)) = v;
         }
       fence_proxy_async_smem();

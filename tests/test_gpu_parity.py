@@ -121,13 +121,14 @@ def test_prefill_full_size_config2_sampled(oracle_mod):
 
 
 # ------------------------------------------------------------------ a7 + a8
-def run_decode(oracle_mod, ctx, n, d, seed=0, steps=1, fragment=0, q_sigma=1.0, max_cache_len=None):
+def run_decode(oracle_mod, ctx, n, d, seed=0, steps=1, fragment=0, q_sigma=1.0, max_cache_len=None,
+               table_cols=0):
     """Prefill (GPU) the first ctx tokens of each sequence, then `steps` decode
     steps; compare each step with the oracle's decode."""
     B = len(ctx)
     hist = [max(c, 1) for c in ctx]
     total = [c + steps for c in ctx]
-    maxb = _ceil(max(total) + 1, BS)
+    maxb = max(_ceil(max(total) + 1, BS), table_cols)
     nblocks = sum(_ceil(t + 1, BS) for t in total) + fragment + 4
     side = Side(oracle_mod, 1, nblocks, n, d)
     if fragment:
@@ -188,8 +189,11 @@ def test_decode_parity(oracle_mod, ctx, n, d):
 
 def test_decode_split_invariance(oracle_mod):
     # the same step planned with a larger max_cache_len uses a different split-K plan
+    plans = {ds.ds_decode_workspace_bytes(2, 2, 128, m) for m in (300, 1500)}
+    assert len(plans) == 2
     for mcl in (None, 1500):
-        _, _, _, errs = run_decode(oracle_mod, [300, 5], 2, 128, seed=3, steps=1, max_cache_len=mcl)
+        _, _, _, errs = run_decode(oracle_mod, [300, 5], 2, 128, seed=3, steps=1, max_cache_len=mcl,
+                                   table_cols=100)
         assert max(errs) <= WARN, (mcl, errs)
 
 
