@@ -9,7 +9,7 @@ requests with OPT-13B attention geometry (40 layers x 40 heads x 128), prompt
   a2+a3  40 x ds_prefill_attn (one per layer, fused paged K/V write)
   a4-a6  ds_kv_migrate of all 40 layers' pages prefill pool -> decode pool
   a7+a8  64 decode steps x 40 layers of ds_decode_attn (append + split-K attention)
-At N=1 one GPU plays both instances (migration is an NCCL SELF send/recv); at
+At N=1 one GPU plays both instances (migration is the LOCAL page copy); at
 N>1 ranks [0, N/2) are prefill instances and [N/2, N) decode instances, paired
 r <-> r + N/2 (independent pairs, one p2p exchange per pair per step; the
 prefill of batch k+1 overlaps the decode of batch k).
@@ -176,58 +176,82 @@ class Engine:
             self.ws = torch.empty(max(16, ds.ds_decode_workspace_bytes(w.B, w.n, w.d, max_c)), dtype=torch.uint8,
                                   device=dev)
         nblk = w.B * w.pages_per_seq
-        mrole = {"both": ds.DS_MIGRATE_SELF, "prefill": ds.DS_MIGRATE_SEND, "decode": ds.DS_MIGRATE_RECV}[role]
+        mrole = {"both": ds.DS_MIGRATE_LOCAL, "prefill": ds.DS_MIGRATE_SEND, "decode": ds.DS_MIGRATE_RECV}[role]
         self.mrole = mrole
         cache_for_size = self.P if self.pf else self.D
-        self.staging = torch.empty(ds.ds_kv_migrate_staging_bytes(cache_for_size, mrole, w.L, nblk, w.n),
-                                   dtype=torch.uint8, device=dev)
+        sbytes = ds.ds_kv_migrate_staging_bytes(cache_for_size, mrole, w.L, nblk, w.n)
+        self.staging = torch.empty(sbytes, dtype=torch.uint8, device=dev) if sbytes else None
+        # pinned host ring for the per-step block-table / cache-length uploads (async H2D)
+        self.ring = w.out_len + 2
+        self.h_tab = torch.empty((self.ring, w.B, w.maxb), dtype=torch.int32).pin_memory()
+        self.h_len = torch.empty((self.ring, w.B), dtype=torch.int32).pin_memory()
+        self.d_tab = torch.empty((self.ring, w.B, w.maxb), dtype=torch.int32, device=dev)
+        self.d_len = torch.empty((self.ring, w.B), dtype=torch.int32, device=dev)
+        self.h_ev = [None] * self.ring
+        self.slot = 0
         self.stream = torch.cuda.current_stream()
         self.launches = 0
         self.decode_events = []
+
+    def upload(self, table: np.ndarray, lens):
+        """async H2D of a block table (+ lengths) through the pinned ring"""
+        s = self.slot
+        self.slot = (s + 1) % self.ring
+        if self.h_ev[s] is not None:
+            self.h_ev[s].synchronize()  # the previous copy out of this slot has completed
+        self.h_tab[s].numpy()[:, :table.shape[1]] = table
+        self.h_len[s].numpy()[:] = lens
+        self.d_tab[s].copy_(self.h_tab[s], non_blocking=True)
+        self.d_len[s].copy_(self.h_len[s], non_blocking=True)
+        ev = self.torch.cuda.Event()
+        ev.record()
+        self.h_ev[s] = ev
+        return self.d_tab[s], self.d_len[s]
 
     # -- one step ------------------------------------------------------------------
     def step(self, events=None, time_decode=False):
         torch, ds, w = self.torch, self.ds, self.w
         ev = events or {}
         nblk = w.B * w.pages_per_seq
+        if "start" in ev:
+            ev["start"].record()
         if self.pf:
-            if "start" in ev:
-                ev["start"].record()
             tp = np.full((w.B, w.maxb), -1, np.int32)
             ds.ds_block_table(self.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
-            tp_d = _i32(torch, tp)
+            tp_d, _ = self.upload(tp, w.lens)
             for layer in range(w.L):
                 ds.ds_prefill_attn(self.q[layer], self.k[layer], self.v[layer], self.out, self.cu, w.l0, self.P, layer,
                                    tp_d, w.scale)
             self.launches += w.L
-            if "prefill_end" in ev:
-                ev["prefill_end"].record()
-            src_ids = _i32(torch, tp[:, :w.pages_per_seq].reshape(-1))
+            src_ids = tp_d[:, :w.pages_per_seq].reshape(-1).contiguous()
+        if "prefill_end" in ev:
+            ev["prefill_end"].record()
         if self.dc:
             td = np.full((w.B, w.maxb), -1, np.int32)
             ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, [0] * w.B, w.lens, td)
-            dst_ids = _i32(torch, td[:, :w.pages_per_seq].reshape(-1))
-        # migration (pull: the decode side has admitted the batch above)
-        if self.mrole == ds.DS_MIGRATE_SELF:
-            ds.ds_kv_migrate(self.comm, self.mrole, 0, self.P, 0, w.L, src_ids, 0, w.n, self.staging,
+            td_d, _ = self.upload(td, w.lens)
+            dst_ids = td_d[:, :w.pages_per_seq].reshape(-1).contiguous()
+        # migration (pull, P:382: the decode side has admitted the batch above)
+        if self.mrole == ds.DS_MIGRATE_LOCAL:
+            ds.ds_kv_migrate(None, self.mrole, 0, self.P, 0, w.L, src_ids, 0, w.n, None,
                              dst_cache=self.D, dst_block_ids=dst_ids)
-        elif self.pf:
-            ds.ds_kv_migrate(self.comm, self.mrole, self.peer, self.P, 0, w.L, src_ids, 0, w.n, self.staging)
+            self.launches += 1
         else:
-            ds.ds_kv_migrate(self.comm, self.mrole, self.peer, self.D, 0, w.L, dst_ids, 0, w.n, self.staging)
-        chunk_rows = max(1, (64 << 20) // (w.n * 16 * w.d * 2))
-        self.launches += (2 if self.mrole == ds.DS_MIGRATE_SELF else 1) * -(-(2 * w.L * nblk) // chunk_rows)
+            chunk_rows = max(1, (64 << 20) // (w.n * 16 * w.d * 2))
+            self.launches += -(-(2 * w.L * nblk) // chunk_rows)  # pack or unpack kernels (+ NCCL's own)
+            if self.pf:
+                ds.ds_kv_migrate(self.comm, self.mrole, self.peer, self.P, 0, w.L, src_ids, 0, w.n, self.staging)
+            else:
+                ds.ds_kv_migrate(self.comm, self.mrole, self.peer, self.D, 0, w.L, dst_ids, 0, w.n, self.staging)
         if self.pf:
             ds.ds_block_table(self.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
         if "migrate_end" in ev:
             ev["migrate_end"].record()
         if self.dc:
             cur = list(w.lens)
-            split = ds.ds_decode_workspace_bytes(w.B, w.n, w.d, w.l0 + w.out_len) > 16
             for s in range(w.out_len):
                 ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, cur, [1] * w.B, td)
-                td_d = _i32(torch, td)
-                cl = _i32(torch, cur)
+                td_d, cl = self.upload(td, cur)
                 for layer in range(w.L):
                     if time_decode:
                         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -237,7 +261,7 @@ class Engine:
                     if time_decode:
                         e1.record()
                         self.decode_events.append((e0, e1, list(cur)))
-                self.launches += w.L * (2 if split else 1)
+                self.launches += 2 * w.L  # decode_kernel + decode_combine_kernel
                 cur = [c + 1 for c in cur]
             ds.ds_block_table(self.pool_d, ds.DS_BT_FREE, cur, None, td)
         if "end" in ev:
@@ -269,10 +293,9 @@ def pair_of(rank, world):
 
 
 def make_comm(world, rank, ds):
-    import torch
     import torch.distributed as dist
     if world == 1:
-        return ds.ds_comm_init(ds.ds_comm_get_unique_id(), 1, 0)
+        return None  # both instances on one GPU: LOCAL page copy, no communicator
     obj = [ds.ds_comm_get_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     return ds.ds_comm_init(obj[0], world, rank)
@@ -450,7 +473,8 @@ def run_ds(args):
                                 "sample": sample}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    comm.close()
+    if comm is not None:
+        comm.close()
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

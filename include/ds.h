@@ -199,7 +199,7 @@ ds_status ds_comm_get_unique_id(void *id_h);
 ds_status ds_comm_init(const void *id_h, int32_t nranks, int32_t rank, ds_comm *out_h);
 ds_status ds_comm_destroy(ds_comm comm);
 
-enum { DS_MIGRATE_SEND = 0, DS_MIGRATE_RECV = 1, DS_MIGRATE_SELF = 2 };
+enum { DS_MIGRATE_SEND = 0, DS_MIGRATE_RECV = 1, DS_MIGRATE_SELF = 2, DS_MIGRATE_LOCAL = 3 };
 
 /* Move whole pages of (layers [layer_begin, +layer_count), head slice
  * [head_begin, +head_count), block_ids[0..num_blocks)) from a prefill rank to
@@ -212,6 +212,9 @@ enum { DS_MIGRATE_SEND = 0, DS_MIGRATE_RECV = 1, DS_MIGRATE_SELF = 2 };
  *  role SELF (one rank plays both, N=1 loopback through NCCL): `cache` is the
  *       source, `dst_cache`/`dst_block_ids`/`dst_head_begin` the destination;
  *       the staging buffer holds two halves (send and receive side).
+ *  role LOCAL (both instances on one device, "asynchronous CudaMemcpy"):
+ *       one kernel copies the pages straight from `cache` to `dst_cache`; no
+ *       communicator (comm may be NULL), no staging (may be NULL / 0).
  * Chunking: the (layer, kv, block) page-rows are moved in chunks of about
  * 64 MiB (at least one row of head_count pages) through a 2-slot ring in the
  * staging buffer (2 send + 2 receive slots for SELF); the pack of chunk k+1

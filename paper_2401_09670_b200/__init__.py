@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_PKG, "libds.so")
 
 DS_OK, DS_ERR_INVALID_ARG, DS_ERR_UNSUPPORTED, DS_ERR_NO_BLOCKS, DS_ERR_CUDA, DS_ERR_NCCL, DS_ERR_STATE = range(7)
 DS_BT_APPEND, DS_BT_FREE = 0, 1
-DS_MIGRATE_SEND, DS_MIGRATE_RECV, DS_MIGRATE_SELF = 0, 1, 2
+DS_MIGRATE_SEND, DS_MIGRATE_RECV, DS_MIGRATE_SELF, DS_MIGRATE_LOCAL = 0, 1, 2, 3
 BLOCK_SIZE = 16
 
 # every symbol include/ds.h declares (checked by tests/test_abi.py)
@@ -315,7 +315,8 @@ def ds_kv_migrate(comm: Comm, role: int, peer: int, cache: KVCache, layer_begin:
     _dev(block_ids, torch.int32, "block_ids")
     if dst_block_ids is not None:
         _dev(dst_block_ids, torch.int32, "dst_block_ids")
-    _check(_lib.ds_kv_migrate(comm._h, role, peer, cache.ref(), layer_begin, layer_count,
+    _check(_lib.ds_kv_migrate(None if comm is None else comm._h, role, peer, cache.ref(), layer_begin, layer_count,
                               block_ids.data_ptr(), block_ids.numel(), head_begin, head_count,
                               None if dst_cache is None else dst_cache.ref(), _ptr(dst_block_ids),
-                              dst_head_begin, staging.data_ptr(), _nbytes(staging), _stream(stream)))
+                              dst_head_begin, _ptr(staging), 0 if staging is None else _nbytes(staging),
+                              _stream(stream)))

@@ -112,20 +112,16 @@ static ds_status cache_map(CUtensorMap *m, const ds_kv_cache *c, const char *whe
 }
 
 // ----------------------------------------------------------- decode planning
-struct DecodePlan {
-  int splits, pages_per_split;
-};
-static DecodePlan plan_decode(int32_t B, int32_t n, int32_t max_c) {
-  const int pages = (max_c + 1 + 15) / 16;
-  const long pairs = (long)B * n;
-  const long target = 148L * 4;  // CTAs to cover the 148 SMs ~4 deep
-  int s = pairs >= target ? 1 : (int)((target + pairs - 1) / pairs);
-  const int max_by_pages = (pages + 3) / 4;  // >= 4 pages (one per warp) per split
-  if (s > max_by_pages) s = max_by_pages;
-  if (s > 64) s = 64;
-  if (s < 1) s = 1;
-  const int pps = (pages + s - 1) / s;
-  return {(pages + pps - 1) / pps, pps};
+static int device_sms() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+    return sms < kDecodeMaxSMs ? sms : kDecodeMaxSMs;
+  return 148;
+}
+// workspace = [kDecodeMaxSMs * warps][2][D+2] floats, then the int32 page prefix [B+1]
+static size_t decode_partials_bytes(int head_dim) {
+  return decode_workspace_bytes(0, head_dim, kDecodeMaxSMs) - 4 - 64;
 }
 
 }  // namespace ds
@@ -180,10 +176,8 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
 
 extern "C" size_t ds_decode_workspace_bytes(int32_t num_seqs, int32_t n_loc, int32_t head_dim,
                                             int32_t max_cache_len) {
-  if (num_seqs <= 0 || n_loc <= 0 || head_dim <= 0 || max_cache_len < 0) return 0;
-  const DecodePlan p = plan_decode(num_seqs, n_loc, max_cache_len);
-  if (p.splits <= 1) return 16;
-  return (size_t)num_seqs * n_loc * p.splits * (head_dim + 2) * sizeof(float);
+  if (num_seqs <= 0 || n_loc <= 0 || (head_dim != 64 && head_dim != 128) || max_cache_len < 0) return 0;
+  return decode_workspace_bytes(num_seqs, head_dim, kDecodeMaxSMs);
 }
 
 extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void *v_new, void *out,
@@ -196,6 +190,8 @@ extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void
   if (num_seqs < 0) return fail(DS_ERR_INVALID_ARG, "%s: num_seqs < 0", W);
   if (ds_status s = check_cache(cache, W)) return s;
   if (num_seqs == 0) return DS_OK;
+  if (num_seqs > kDecodeMaxSeqs)
+    return fail(DS_ERR_INVALID_ARG, "%s: at most %d sequences per call", W, kDecodeMaxSeqs);
   if (!q || !k_new || !v_new || !out || !block_table || !cache_lens)
     return fail(DS_ERR_INVALID_ARG, "%s: NULL pointer argument", W);
   if (!aligned16(q) || !aligned16(k_new) || !aligned16(v_new) || !aligned16(out))
@@ -206,9 +202,8 @@ extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void
   if (!(softmax_scale > 0.f) || !isfinite(softmax_scale))
     return fail(DS_ERR_INVALID_ARG, "%s: softmax_scale must be finite and > 0", W);
   const int D = cache->head_dim, n = cache->num_heads;
-  const DecodePlan p = plan_decode(num_seqs, n, max_cache_len);
   const size_t need = ds_decode_workspace_bytes(num_seqs, n, D, max_cache_len);
-  if (p.splits > 1 && (!workspace || workspace_bytes < need || !aligned16(workspace)))
+  if (!workspace || workspace_bytes < need || !aligned16(workspace))
     return fail(DS_ERR_INVALID_ARG, "%s: workspace must be >= %zu bytes and 16-B aligned", W, need);
   if (ds_status s = require_sm100(W)) return s;
   DecodeArgs a{};
@@ -220,15 +215,14 @@ extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void
   a.block_table = block_table;
   a.cache_lens = cache_lens;
   a.workspace = static_cast<float *>(workspace);
+  a.ws_prefix = reinterpret_cast<int32_t *>(static_cast<char *>(workspace) + decode_partials_bytes(D));
   a.layer = layer;
   a.num_blocks = cache->num_blocks;
   a.n_loc = n;
   a.max_blocks = max_blocks_per_seq;
   a.num_seqs = num_seqs;
-  a.num_splits = p.splits;
-  a.pages_per_split = p.pages_per_split;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
-  cudaError_t e = launch_decode(a, D, static_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_decode(a, D, device_sms(), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, W);
   return DS_OK;
 }

@@ -5,19 +5,23 @@
 // whole cached K/V once per step). Reading R9: the new token's K/V are appended
 // at position c before attending, so the step attends c+1 tokens.
 //
-// B200 design (HBM-bound, no tensor cores — each cached element is used once):
-//  * one CTA of 4 warps per (sequence, head, split); a split is a contiguous
-//    range of 16-token pages; splits are only used when B*n_loc cannot fill the
-//    148 SMs, and their partials are merged by a log-sum-exp combine (a8);
-//  * each warp owns whole pages: its lanes form 32/TPG token groups of TPG =
-//    head_dim/8 lanes; a lane loads 16 B (8 bf16) of a K row and of a V row
-//    with 128-bit non-allocating loads, all 2x(16/ (32/TPG)) loads of a page
-//    issued before use (one page of K and V = 8 KiB in flight per warp);
-//  * q.k partial dots are reduced with xor-shuffles inside the TPG-lane group;
-//    online softmax in base 2 (scale*log2 e folded into q), one rescale per
-//    page; groups, warps and splits are merged with the same (m, l, o) rule.
-//  * the append (i) is fused: the CTA whose split holds position c writes
-//    k_new/v_new into the page and uses them from registers for token c.
+// B200 design (HBM-bound; no tensor cores — every cached element is used once):
+//  * persistent grid of one 8-warp CTA per SM; the (sequence, head, page) space
+//    is flattened and cut into equal contiguous page ranges, one per warp, so
+//    every warp streams the same number of pages whatever the batch and length
+//    mix (no wave tail, no idle SMs on ragged batches);
+//  * each warp keeps its own ring of NSTAGE (K page, V page) smem stages filled
+//    by 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx) issued by one
+//    lane NSTAGE pages ahead: 8 warps x 3 x 8 KiB = 192 KiB in flight per SM;
+//  * consumer: a 16-token page is read from smem by TPG = head_dim/8 lanes per
+//    token row (16-B vectors, conflict-free), q.k partials reduced with xor
+//    shuffles, online softmax in base 2 (scale*log2 e folded into q), one
+//    rescale per page;
+//  * a warp's range covers whole (seq, head) pairs — written straight to `out`
+//    — plus at most a partial first and a partial last pair, whose (m, l, o)
+//    go to the workspace and are merged by decode_combine_kernel (a8);
+//  * the append (i) is fused: the warp that owns the page holding position c
+//    stores k_new/v_new into it and uses them from global memory for token c.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -25,16 +29,20 @@ namespace ds {
 
 namespace {
 
-constexpr int kWarps = 4;
+constexpr int kWarps = 8;
+constexpr int kMaxSeqs = kDecodeMaxSeqs;
 constexpr float kNegInf = -__builtin_huge_valf();
 
-DS_DEVICE uint4 ld_nc_v4(const void *p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
-}
+template <int D>
+struct DecCfg {
+  static constexpr int kPageBytes = 16 * D * 2;
+  static constexpr int kStageBytes = 2 * kPageBytes;  // K page + V page
+  static constexpr int kStages = D == 128 ? 3 : 6;
+  static constexpr int kRingBytes = kWarps * kStages * kStageBytes;
+  static constexpr int kPrefixOff = kRingBytes;  // int[kMaxSeqs + 1]
+  static constexpr int kBarOff = (kPrefixOff + (kMaxSeqs + 1) * 4 + 7) & ~7;
+  static constexpr int kSmem = kBarOff + kWarps * kStages * 8;
+};
 
 DS_DEVICE float dot8(const float (&q)[8], const uint4 &k) {
   float s = q[0] * bf16lo(k.x);
@@ -62,83 +70,179 @@ DS_DEVICE void axpy8(float (&acc)[8], float p, const uint4 &v) {
 // weight of a partial with running max m against merged max mm (0 if empty)
 DS_DEVICE float rescale(float m, float mm) { return m == kNegInf ? 0.f : ex2(m - mm); }
 
+DS_DEVICE int npages_of(int c) { return (c + 1 + 15) >> 4; }
+
+// page range [B_w, B_{w+1}) of warp w out of W over P pages
+__host__ __device__ inline int64_t range_begin(int64_t w, int64_t W, int64_t P) { return w * P / W; }
+
+// exclusive prefix of pages per sequence: prefix[b] = sum_{b' < b} npages(b')
+DS_DEVICE void build_prefix(const int32_t *cache_lens, int B, int *prefix) {
+  __shared__ int partial[kWarps * 32];
+  const int T = blockDim.x, t = threadIdx.x;
+  const int per = (B + T - 1) / T;
+  const int b0 = min(B, t * per), b1 = min(B, b0 + per);
+  int s = 0;
+  for (int b = b0; b < b1; ++b) s += npages_of(cache_lens[b]);
+  partial[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    int run = 0;
+    for (int i = 0; i < T; ++i) {
+      const int v = partial[i];
+      partial[i] = run;
+      run += v;
+    }
+    prefix[B] = run;
+  }
+  __syncthreads();
+  int run = partial[t];
+  for (int b = b0; b < b1; ++b) {
+    prefix[b] = run;
+    run += npages_of(cache_lens[b]);
+  }
+  __syncthreads();
+}
+
+// flattened page x -> (b, h, p); order (b, h, p): the pages of head h of
+// sequence b are contiguous in the flattened space.
+struct PagePos {
+  int b, h, p, npg;
+};
+DS_DEVICE PagePos locate(int64_t x, const int *prefix, int B, int n) {
+  int lo = 0, hi = B - 1;  // largest b with n*prefix[b] <= x
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((int64_t)n * prefix[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  const int npg = prefix[lo + 1] - prefix[lo];
+  const int64_t off = x - (int64_t)n * prefix[lo];
+  return {lo, (int)(off / npg), (int)(off % npg), npg};
+}
+DS_DEVICE void advance(PagePos &q, const int *prefix, int n) {
+  if (++q.p == q.npg) {
+    q.p = 0;
+    if (++q.h == n) {
+      q.h = 0;
+      ++q.b;
+      q.npg = prefix[q.b + 1] - prefix[q.b];
+    }
+  }
+}
+
 template <int D>
-__global__ void __launch_bounds__(kWarps * 32)
-    decode_split_kernel(const DecodeArgs a) {
-  constexpr int TPG = D / 8;        // lanes per token row
-  constexpr int GPW = 32 / TPG;     // token groups per warp
-  constexpr int NIT = 16 / GPW;     // loads per lane per page (K and V each)
-  const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+__global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs a) {
+  using C = DecCfg<D>;
+  constexpr int TPG = D / 8;     // lanes per token row
+  constexpr int GPW = 32 / TPG;  // token rows per warp instruction
+  constexpr int NIT = 16 / GPW;  // rows per lane per page
+  extern __shared__ __align__(128) uint8_t smem[];
+  int *prefix = reinterpret_cast<int *>(smem + C::kPrefixOff);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::kBarOff);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / TPG, dpart = lane % TPG;
+  const int B = a.num_seqs, n = a.n_loc;
 
-  const int c = a.cache_lens[b];
-  const int npages = (c + 1 + 15) >> 4;
-  const int p_begin = split * a.pages_per_split;
-  const int p_end = min(npages, p_begin + a.pages_per_split);
-  if (p_begin >= p_end) return;  // empty split (combine skips it)
+  build_prefix(a.cache_lens, B, prefix);
+  if (blockIdx.x == 0) {  // publish the plan for the combine kernel
+    for (int b = threadIdx.x; b <= B; b += blockDim.x) a.ws_prefix[b] = prefix[b];
+  }
+  const int64_t P = (int64_t)n * prefix[B];
+  const int64_t W = (int64_t)gridDim.x * kWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t x0 = range_begin(gw, W, P), x1 = range_begin(gw + 1, W, P);
+  if (x0 >= x1) return;
 
-  const int n = a.n_loc;
-  const size_t row_off = ((size_t)b * n + h) * D;  // [B][n][D]
+  uint8_t *ring = smem + warp * C::kStages * C::kStageBytes;
+  uint64_t *wbar = bars + warp * C::kStages;
+  if (lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) mbar_init(&wbar[s], 1);
+    fence_barrier_init();
+  }
+  __syncwarp();
+
   const size_t page_elems = 16 * D;
   const size_t kv_stride = (size_t)a.num_blocks * n * page_elems;  // K -> V
   const uint16_t *layer_base = a.cache + (size_t)a.layer * 2 * kv_stride;
-  const int *bt = a.block_table + (size_t)b * a.max_blocks;
-  const int c_page = c >> 4;
 
-  // (i) fused append of the new token's K/V at position c (R9)
-  if (c_page >= p_begin && c_page < p_end && warp == 0 && lane < 2 * TPG) {
-    const int kv = lane / TPG, part = lane % TPG;
-    const uint16_t *src = (kv ? a.v_new : a.k_new) + row_off + part * 8;
-    uint16_t *dst = const_cast<uint16_t *>(layer_base) + kv * kv_stride +
-                    ((size_t)bt[c_page] * n + h) * page_elems + (size_t)(c & 15) * D + part * 8;
-    *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(src);
-  }
+  // producer (lane 0): TMA bulk copies NSTAGE pages ahead of the consumer
+  PagePos pq = locate(x0, prefix, B, n);
+  int64_t issued = x0;
+  auto issue = [&](int stage) {
+    const int blk = a.block_table[(size_t)pq.b * a.max_blocks + pq.p];
+    const uint16_t *kp = layer_base + ((size_t)blk * n + pq.h) * page_elems;
+    uint8_t *dst = ring + stage * C::kStageBytes;
+    mbar_arrive_expect_tx(&wbar[stage], C::kStageBytes);
+    bulk_g2s(dst, kp, C::kPageBytes, &wbar[stage]);
+    bulk_g2s(dst + C::kPageBytes, kp + kv_stride, C::kPageBytes, &wbar[stage]);
+    advance(pq, prefix, n);
+    ++issued;
+  };
+  if (lane == 0)
+    for (int s = 0; s < C::kStages && issued < x1; ++s) issue(s);
 
-  float q[8];
-  {
-    const uint4 qv = *reinterpret_cast<const uint4 *>(a.q + row_off + dpart * 8);
+  // consumer
+  PagePos cq = locate(x0, prefix, B, n);
+  int seg_begin = cq.p;  // the first segment may start mid-pair
+  bool first_seg = true;
+  float q[8], m = kNegInf, l = 0.f, acc[8];
+  int c = 0;
+  auto load_pair = [&]() {
+    const size_t row = ((size_t)cq.b * n + cq.h) * D + dpart * 8;
+    const uint4 qv = *reinterpret_cast<const uint4 *>(a.q + row);
     const float s = a.scale_log2;
     q[0] = bf16lo(qv.x) * s; q[1] = bf16hi(qv.x) * s;
     q[2] = bf16lo(qv.y) * s; q[3] = bf16hi(qv.y) * s;
     q[4] = bf16lo(qv.z) * s; q[5] = bf16hi(qv.z) * s;
     q[6] = bf16lo(qv.w) * s; q[7] = bf16hi(qv.w) * s;
-  }
-  const uint16_t *knew = a.k_new + row_off + dpart * 8;
-  const uint16_t *vnew = a.v_new + row_off + dpart * 8;
-
-  float m = kNegInf, l = 0.f, acc[8];
+    c = a.cache_lens[cq.b];
+    m = kNegInf;
+    l = 0.f;
 #pragma unroll
-  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  };
+  load_pair();
 
-  for (int p = p_begin + warp; p < p_end; p += kWarps) {
-    const size_t pg = ((size_t)bt[p] * n + h) * page_elems;
-    const uint16_t *kp = layer_base + pg + dpart * 8;
-    const uint16_t *vp = layer_base + kv_stride + pg + dpart * 8;
+  for (int64_t x = x0; x < x1; ++x) {
+    const int it_idx = (int)(x - x0);
+    const int stage = it_idx % C::kStages;
+    const size_t row = ((size_t)cq.b * n + cq.h) * D + dpart * 8;
+    // (i) fused append: the owner of the page holding position c stores the new token
+    if (cq.p == (c >> 4) && lane < 2 * TPG) {
+      const int kv = lane / TPG;
+      const size_t r2 = ((size_t)cq.b * n + cq.h) * D + (lane % TPG) * 8;
+      const int blk = a.block_table[(size_t)cq.b * a.max_blocks + cq.p];
+      uint16_t *dst = const_cast<uint16_t *>(layer_base) + kv * kv_stride +
+                      ((size_t)blk * n + cq.h) * page_elems + (size_t)(c & 15) * D + (lane % TPG) * 8;
+      *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>((kv ? a.v_new : a.k_new) + r2);
+    }
+    mbar_wait(&wbar[stage], (it_idx / C::kStages) & 1);
+    const uint8_t *kst = ring + stage * C::kStageBytes;
+    const uint8_t *vst = kst + C::kPageBytes;
     uint4 kr[NIT], vr[NIT];
 #pragma unroll
     for (int it = 0; it < NIT; ++it) {
-      const int t = it * GPW + g, pos = p * 16 + t;
-      const bool is_new = pos == c;
-      kr[it] = is_new ? *reinterpret_cast<const uint4 *>(knew)
-                      : ld_nc_v4(kp + (size_t)t * D);
+      const int t = it * GPW + g;
+      const bool is_new = cq.p * 16 + t == c;
+      kr[it] = is_new ? *reinterpret_cast<const uint4 *>(a.k_new + row)
+                      : *reinterpret_cast<const uint4 *>(kst + t * (D * 2) + dpart * 16);
+      vr[it] = is_new ? *reinterpret_cast<const uint4 *>(a.v_new + row)
+                      : *reinterpret_cast<const uint4 *>(vst + t * (D * 2) + dpart * 16);
     }
-#pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-      const int t = it * GPW + g, pos = p * 16 + t;
-      const bool is_new = pos == c;
-      vr[it] = is_new ? *reinterpret_cast<const uint4 *>(vnew)
-                      : ld_nc_v4(vp + (size_t)t * D);
+    // the stage is consumed (values are in registers): refill it NSTAGE pages ahead
+    __syncwarp();
+    if (lane == 0 && issued < x1) {
+      fence_proxy_async_smem();
+      issue(stage);
     }
     float s[NIT];
     float pmax = kNegInf;
 #pragma unroll
     for (int it = 0; it < NIT; ++it) {
-      float x = dot8(q, kr[it]);
+      float xv = dot8(q, kr[it]);
 #pragma unroll
-      for (int off = TPG / 2; off >= 1; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off);
-      const int pos = p * 16 + it * GPW + g;
-      s[it] = pos <= c ? x : kNegInf;
+      for (int off = TPG / 2; off >= 1; off >>= 1) xv += __shfl_xor_sync(0xffffffffu, xv, off);
+      s[it] = (cq.p * 16 + it * GPW + g) <= c ? xv : kNegInf;
       pmax = fmaxf(pmax, s[it]);
     }
     const float m_new = fmaxf(m, pmax);
@@ -157,94 +261,124 @@ __global__ void __launch_bounds__(kWarps * 32)
       }
       m = m_new;
     }
-  }
-
-  // merge the GPW token groups of the warp (lanes with equal ds)
+    // end of a segment: this pair's pages inside our range are done
+    const bool pair_end = cq.p == cq.npg - 1;
+    if (pair_end || x == x1 - 1) {
 #pragma unroll
-  for (int off = TPG; off < 32; off <<= 1) {
-    const float mo = __shfl_xor_sync(0xffffffffu, m, off);
-    const float lo = __shfl_xor_sync(0xffffffffu, l, off);
-    const float mm = fmaxf(m, mo);
-    const float wa = rescale(m, mm), wb = rescale(mo, mm);
-    l = l * wa + lo * wb;
+      for (int off = TPG; off < 32; off <<= 1) {  // merge the GPW token-row groups
+        const float mo = __shfl_xor_sync(0xffffffffu, m, off);
+        const float lo = __shfl_xor_sync(0xffffffffu, l, off);
+        const float mm = fmaxf(m, mo);
+        const float wa = rescale(m, mm), wb = rescale(mo, mm);
+        l = l * wa + lo * wb;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float ao = __shfl_xor_sync(0xffffffffu, acc[e], off);
-      acc[e] = acc[e] * wa + ao * wb;
-    }
-    m = mm;
-  }
-
-  // merge the warps through shared memory
-  __shared__ float s_o[kWarps][D];
-  __shared__ float s_ml[kWarps][2];
-  if (lane < TPG) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) s_o[warp][dpart * 8 + e] = acc[e];
-    if (lane == 0) {
-      s_ml[warp][0] = m;
-      s_ml[warp][1] = l;
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < D) {
-    const int t = threadIdx.x;
-    float mm = kNegInf;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) mm = fmaxf(mm, s_ml[w][0]);
-    float lt = 0.f, ot = 0.f;
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const float wt = rescale(s_ml[w][0], mm);
-      lt += s_ml[w][1] * wt;
-      ot += s_o[w][t] * wt;
-    }
-    if (a.num_splits == 1) {
-      reinterpret_cast<__nv_bfloat16 *>(a.out)[row_off + t] = __float2bfloat16_rn(ot / lt);
-    } else {
-      float *ws = a.workspace + (((size_t)b * n + h) * a.num_splits + split) * (D + 2);
-      ws[t] = ot;
-      if (t == 0) {
-        ws[D] = mm;
-        ws[D + 1] = lt;
+        for (int e = 0; e < 8; ++e) {
+          const float ao = __shfl_xor_sync(0xffffffffu, acc[e], off);
+          acc[e] = acc[e] * wa + ao * wb;
+        }
+        m = mm;
       }
+      if (seg_begin == 0 && pair_end) {  // the whole pair is ours: final output
+        if (lane < TPG) {
+          const float inv = 1.f / l;
+          uint4 o;
+          o.x = pack_bf16(acc[0] * inv, acc[1] * inv);
+          o.y = pack_bf16(acc[2] * inv, acc[3] * inv);
+          o.z = pack_bf16(acc[4] * inv, acc[5] * inv);
+          o.w = pack_bf16(acc[6] * inv, acc[7] * inv);
+          *reinterpret_cast<uint4 *>(reinterpret_cast<uint16_t *>(a.out) + row) = o;
+        }
+      } else {  // a straddling pair: partial (o, m, l) for the combine
+        float *ws = a.workspace + ((size_t)gw * 2 + (first_seg ? 0 : 1)) * (D + 2);
+        if (lane < TPG) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) ws[dpart * 8 + e] = acc[e];
+          if (lane == 0) {
+            ws[D] = m;
+            ws[D + 1] = l;
+          }
+        }
+      }
+      first_seg = false;
+      if (x + 1 < x1) {
+        advance(cq, prefix, n);
+        seg_begin = 0;
+        load_pair();
+      }
+    } else {
+      advance(cq, prefix, n);
     }
   }
 }
 
-// a8: log-sum-exp merge of the split partials:
+// a8: merge the partials of the pairs that straddle warp ranges:
 //   m* = max_k m_k ; l* = sum_k l_k 2^(m_k - m*) ; o = sum_k o_k 2^(m_k - m*) / l*
 template <int D>
-__global__ void __launch_bounds__(D) decode_combine_kernel(const DecodeArgs a) {
-  const int h = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
-  const int c = a.cache_lens[b];
-  const int npages = (c + 1 + 15) >> 4;
-  const int active = (npages + a.pages_per_split - 1) / a.pages_per_split;
-  const float *ws = a.workspace + ((size_t)b * a.n_loc + h) * a.num_splits * (D + 2);
+__global__ void __launch_bounds__(128) decode_combine_kernel(const DecodeArgs a, int warps_total) {
+  const int n = a.n_loc, B = a.num_seqs;
+  const int pair = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (pair >= B * n) return;
+  const int lane = threadIdx.x & 31;
+  const int b = pair / n, h = pair % n;
+  const int *prefix = a.ws_prefix;
+  const int64_t P = (int64_t)n * prefix[B];
+  const int npg = prefix[b + 1] - prefix[b];
+  const int64_t start = (int64_t)n * prefix[b] + (int64_t)h * npg, last = start + npg - 1;
+  const int64_t W = warps_total;
+  auto owner = [&](int64_t x) {
+    int64_t w = x * W / P;
+    while (w + 1 < W && range_begin(w + 1, W, P) <= x) ++w;
+    while (w > 0 && range_begin(w, W, P) > x) --w;
+    return w;
+  };
+  const int64_t w0 = owner(start), w1 = owner(last);
+  if (w0 == w1) return;  // written directly by its warp
+  constexpr int PER = D / 32;
+  const int slot0 = range_begin(w0, W, P) < start ? 1 : 0;  // pair is w0's last segment
   float mm = kNegInf;
-  for (int k = 0; k < active; ++k) mm = fmaxf(mm, ws[k * (D + 2) + D]);
-  float lt = 0.f, ot = 0.f;
-  for (int k = 0; k < active; ++k) {
-    const float w = rescale(ws[k * (D + 2) + D], mm);
-    lt += ws[k * (D + 2) + D + 1] * w;
-    ot += ws[k * (D + 2) + t] * w;
+  for (int64_t w = w0; w <= w1; ++w)
+    mm = fmaxf(mm, a.workspace[((size_t)w * 2 + (w == w0 ? slot0 : 0)) * (D + 2) + D]);
+  float lt = 0.f, ot[PER];
+#pragma unroll
+  for (int e = 0; e < PER; ++e) ot[e] = 0.f;
+  for (int64_t w = w0; w <= w1; ++w) {
+    const float *ws = a.workspace + ((size_t)w * 2 + (w == w0 ? slot0 : 0)) * (D + 2);
+    const float wt = rescale(ws[D], mm);
+    lt += ws[D + 1] * wt;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) ot[e] += ws[lane * PER + e] * wt;
   }
-  reinterpret_cast<__nv_bfloat16 *>(a.out)[((size_t)b * a.n_loc + h) * D + t] =
-      __float2bfloat16_rn(ot / lt);
+  const float inv = 1.f / lt;
+  uint16_t *o = reinterpret_cast<uint16_t *>(a.out) + ((size_t)b * n + h) * D + lane * PER;
+#pragma unroll
+  for (int e = 0; e < PER; e += 2)
+    *reinterpret_cast<uint32_t *>(o + e) = pack_bf16(ot[e] * inv, ot[e + 1] * inv);
 }
 
 }  // namespace
 
-cudaError_t launch_decode(const DecodeArgs &a, int head_dim, cudaStream_t stream) {
-  dim3 grid(a.num_splits, a.n_loc, a.num_seqs);
+size_t decode_workspace_bytes(int num_seqs, int head_dim, int num_sms) {
+  return (size_t)num_sms * kWarps * 2 * (head_dim + 2) * sizeof(float) + (size_t)(num_seqs + 1) * 4 + 64;
+}
+
+int decode_warps_per_cta() { return kWarps; }
+
+cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaStream_t stream) {
+  const int warps_total = num_sms * kWarps;
+  const int combine_blocks = (a.num_seqs * a.n_loc + 3) / 4;
+  cudaError_t e;
   if (head_dim == 128) {
-    decode_split_kernel<128><<<grid, kWarps * 32, 0, stream>>>(a);
-    if (a.num_splits > 1)
-      decode_combine_kernel<128><<<dim3(a.n_loc, a.num_seqs), 128, 0, stream>>>(a);
+    const int smem = DecCfg<128>::kSmem;
+    e = cudaFuncSetAttribute(decode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    decode_kernel<128><<<num_sms, kWarps * 32, smem, stream>>>(a);
+    decode_combine_kernel<128><<<combine_blocks, 128, 0, stream>>>(a, warps_total);
   } else {
-    decode_split_kernel<64><<<grid, kWarps * 32, 0, stream>>>(a);
-    if (a.num_splits > 1)
-      decode_combine_kernel<64><<<dim3(a.n_loc, a.num_seqs), 64, 0, stream>>>(a);
+    const int smem = DecCfg<64>::kSmem;
+    e = cudaFuncSetAttribute(decode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    decode_kernel<64><<<num_sms, kWarps * 32, smem, stream>>>(a);
+    decode_combine_kernel<64><<<combine_blocks, 128, 0, stream>>>(a, warps_total);
   }
   return cudaGetLastError();
 }

@@ -9,18 +9,21 @@
 namespace ds {
 
 // a7 + a8
+constexpr int kDecodeMaxSeqs = 4096;  // sequences per decode launch (smem page prefix)
+constexpr int kDecodeMaxSMs = 160;    // workspace is sized for grids up to this many CTAs
 struct DecodeArgs {
   const uint16_t *q, *k_new, *v_new;  // bf16 [B][n][D]
   void *out;                          // bf16 [B][n][D]
   const uint16_t *cache;              // pool base [L][2][NB][n][16][D]
   const int32_t *block_table;         // [B][max_blocks]
   const int32_t *cache_lens;          // [B]
-  float *workspace;                   // [B][n][splits][D+2]
+  float *workspace;                   // [warps][2][D+2] straddling-pair partials
+  int32_t *ws_prefix;                 // [B+1] page prefix published for the combine
   int32_t layer, num_blocks, n_loc, max_blocks, num_seqs;
-  int32_t num_splits, pages_per_split;
   float scale_log2;  // softmax_scale * log2(e)
 };
-cudaError_t launch_decode(const DecodeArgs &a, int head_dim, cudaStream_t stream);
+size_t decode_workspace_bytes(int num_seqs, int head_dim, int num_sms);
+cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaStream_t stream);
 
 // a4 / a6: page rows <-> staging
 struct KvCopyArgs {
@@ -32,6 +35,16 @@ struct KvCopyArgs {
   int64_t row_begin, row_end;  // rows of (layer, kv, i) to copy, staging row r at r - row_begin
 };
 cudaError_t launch_kv_copy(const KvCopyArgs &a, bool pack, cudaStream_t stream);
+
+// a4+a5+a6 on one device (LOCAL): pool pages -> pool pages
+struct KvLocalArgs {
+  const uint16_t *src;
+  uint16_t *dst;
+  const int32_t *src_ids, *dst_ids;  // [num_blocks_sel]
+  int32_t layer_begin, layer_count, num_blocks_sel, head_count, head_dim;
+  int32_t src_blocks, src_heads, src_head0, dst_blocks, dst_heads, dst_head0;
+};
+cudaError_t launch_kv_local(const KvLocalArgs &a, cudaStream_t stream);
 
 // a2 + a3
 struct PrefillArgs {

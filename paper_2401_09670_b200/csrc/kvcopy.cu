@@ -64,7 +64,50 @@ __global__ void __launch_bounds__(kThreads) kv_copy_kernel(const KvCopyArgs a) {
   }
 }
 
+// LOCAL migration (both instances on one device): pool row -> pool row directly,
+// no staging buffer and no NCCL ("asynchronous CudaMemcpy" intra-device).
+__global__ void __launch_bounds__(kThreads) kv_local_kernel(const KvLocalArgs a) {
+  const int64_t page_bytes = 16LL * a.head_dim * 2;
+  const int64_t row_bytes = page_bytes * a.head_count;
+  const int64_t segs_per_row = (row_bytes + kSegBytes - 1) / kSegBytes;
+  const int64_t rows = 2LL * a.layer_count * a.num_blocks_sel;
+  const int64_t items = rows * segs_per_row;
+  const int64_t src_kv = (int64_t)a.src_blocks * a.src_heads * page_bytes;
+  const int64_t dst_kv = (int64_t)a.dst_blocks * a.dst_heads * page_bytes;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t r = it / segs_per_row, seg = it % segs_per_row;
+    const int64_t i = r % a.num_blocks_sel;
+    const int64_t kv = (r / a.num_blocks_sel) & 1;
+    const int64_t layer = a.layer_begin + r / (2LL * a.num_blocks_sel);
+    const char *src = reinterpret_cast<const char *>(a.src) + (2 * layer + kv) * src_kv +
+                      ((int64_t)a.src_ids[i] * a.src_heads + a.src_head0) * page_bytes;
+    char *dst = reinterpret_cast<char *>(a.dst) + (2 * layer + kv) * dst_kv +
+                ((int64_t)a.dst_ids[i] * a.dst_heads + a.dst_head0) * page_bytes;
+    const int64_t base = seg * kSegBytes;
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t off = base + ((int64_t)u * kThreads + threadIdx.x) * 16;
+      if (off < row_bytes) v[u] = ld_stream(reinterpret_cast<const uint4 *>(src + off));
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t off = base + ((int64_t)u * kThreads + threadIdx.x) * 16;
+      if (off < row_bytes) *reinterpret_cast<uint4 *>(dst + off) = v[u];
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_kv_local(const KvLocalArgs &a, cudaStream_t stream) {
+  const int64_t row_bytes = 16LL * a.head_dim * 2 * a.head_count;
+  const int64_t items = 2LL * a.layer_count * a.num_blocks_sel * ((row_bytes + kSegBytes - 1) / kSegBytes);
+  if (items <= 0) return cudaSuccess;
+  const int grid = (int)(items < 148LL * 8 ? items : 148LL * 8);
+  kv_local_kernel<<<grid, kThreads, 0, stream>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_kv_copy(const KvCopyArgs &a, bool pack, cudaStream_t stream) {
   const int64_t row_bytes = 16LL * a.head_dim * 2 * a.head_count;

@@ -79,6 +79,7 @@ extern "C" size_t ds_kv_migrate_staging_bytes(const ds_kv_cache *cache, int32_t 
   if (!cache || layer_count <= 0 || num_blocks <= 0 || head_count <= 0) return 0;
   const int64_t row_bytes = (int64_t)head_count * 16 * cache->head_dim * 2;
   const int64_t rows = (int64_t)layer_count * 2 * num_blocks;
+  if (role == DS_MIGRATE_LOCAL) return 0;
   const int64_t slots = role == DS_MIGRATE_SELF ? 4 : 2;
   return (size_t)(slots * chunk_rows_for(row_bytes, rows) * row_bytes);
 }
@@ -136,6 +137,49 @@ extern "C" ds_status ds_comm_destroy(ds_comm c) {
   return DS_OK;
 }
 
+static ds_status migrate_local(const ds_kv_cache *src, int32_t layer_begin, int32_t layer_count,
+                               const int32_t *src_ids, int32_t num_blocks, int32_t src_h0,
+                               int32_t head_count, const ds_kv_cache *dst, const int32_t *dst_ids,
+                               int32_t dst_h0, void *stream) {
+  const char *W = "ds_kv_migrate(LOCAL)";
+  if (!src || !dst) return fail(DS_ERR_INVALID_ARG, "%s: NULL cache", W);
+  if (layer_count < 0 || num_blocks < 0 || head_count < 0)
+    return fail(DS_ERR_INVALID_ARG, "%s: negative count", W);
+  const ds_kv_cache *ends[2] = {src, dst};
+  const int32_t h0s[2] = {src_h0, dst_h0};
+  for (int e = 0; e < 2; ++e) {
+    const ds_kv_cache *c = ends[e];
+    if (!c->base || c->block_size != 16 || (c->head_dim != 64 && c->head_dim != 128))
+      return fail(DS_ERR_INVALID_ARG, "%s: bad cache descriptor", W);
+    if (layer_begin < 0 || layer_begin + layer_count > c->num_layers)
+      return fail(DS_ERR_INVALID_ARG, "%s: layer range outside the pool", W);
+    if (h0s[e] < 0 || h0s[e] + head_count > c->num_heads)
+      return fail(DS_ERR_INVALID_ARG, "%s: head slice outside n_loc", W);
+  }
+  if (src->head_dim != dst->head_dim) return fail(DS_ERR_INVALID_ARG, "%s: head_dim differs", W);
+  if ((int64_t)layer_count * num_blocks * head_count == 0) return DS_OK;
+  if (!src_ids || !dst_ids) return fail(DS_ERR_INVALID_ARG, "%s: NULL block ids", W);
+  KvLocalArgs a{};
+  a.src = static_cast<const uint16_t *>(src->base);
+  a.dst = static_cast<uint16_t *>(dst->base);
+  a.src_ids = src_ids;
+  a.dst_ids = dst_ids;
+  a.layer_begin = layer_begin;
+  a.layer_count = layer_count;
+  a.num_blocks_sel = num_blocks;
+  a.head_count = head_count;
+  a.head_dim = src->head_dim;
+  a.src_blocks = src->num_blocks;
+  a.src_heads = src->num_heads;
+  a.src_head0 = src_h0;
+  a.dst_blocks = dst->num_blocks;
+  a.dst_heads = dst->num_heads;
+  a.dst_head0 = dst_h0;
+  cudaError_t e = launch_kv_local(a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(DS_ERR_CUDA, "%s: %s", W, cudaGetErrorString(e));
+  return DS_OK;
+}
+
 extern "C" ds_status ds_kv_migrate(ds_comm comm, int32_t role, int32_t peer,
                                    const ds_kv_cache *cache, int32_t layer_begin,
                                    int32_t layer_count, const int32_t *block_ids,
@@ -144,6 +188,9 @@ extern "C" ds_status ds_kv_migrate(ds_comm comm, int32_t role, int32_t peer,
                                    int32_t dst_head_begin, void *staging, size_t staging_bytes,
                                    void *stream) {
   const char *W = "ds_kv_migrate";
+  if (role == DS_MIGRATE_LOCAL) return migrate_local(cache, layer_begin, layer_count, block_ids, num_blocks,
+                                                     head_begin, head_count, dst_cache, dst_block_ids,
+                                                     dst_head_begin, stream);
   if (!comm || !comm->comm) return fail(DS_ERR_STATE, "%s: invalid communicator", W);
   if (role != DS_MIGRATE_SEND && role != DS_MIGRATE_RECV && role != DS_MIGRATE_SELF)
     return fail(DS_ERR_INVALID_ARG, "%s: bad role", W);

@@ -54,8 +54,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tm_cache, const PrefillArgs a) {
   using S = Smem<D>;
   constexpr int kChunks = D / 64;
-  const int h = blockIdx.x, r = blockIdx.y;
-  const int i = a.num_q_tiles - 1 - (int)blockIdx.z;  // heaviest (longest causal row) first
+  // q tiles of one (sequence, head) are adjacent in launch order so their K/V
+  // re-reads hit L2; within the group the heaviest (longest causal row) goes first
+  const int h = blockIdx.y, r = blockIdx.z;
+  const int i = a.num_q_tiles - 1 - (int)blockIdx.x;
   const int seq_start = a.cu_seqlens[r];
   const int len = a.cu_seqlens[r + 1] - seq_start;
   if (i * kBM >= len) return;
@@ -288,7 +290,7 @@ size_t prefill_smem_bytes(int head_dim) {
 cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
                            const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
                            cudaStream_t stream) {
-  dim3 grid(a.n_loc, a.num_seqs, a.num_q_tiles);
+  dim3 grid(a.num_q_tiles, a.n_loc, a.num_seqs);
   const size_t smem = prefill_smem_bytes(head_dim);
   cudaError_t e;
   if (head_dim == 128) {
