@@ -10,13 +10,16 @@
 //    is flattened and cut into equal contiguous page ranges, one per warp, so
 //    every warp streams the same number of pages whatever the batch and length
 //    mix (no wave tail, no idle SMs on ragged batches);
-//  * each warp keeps its own ring of NSTAGE (K page, V page) smem stages filled
-//    by 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx) issued by one
-//    lane NSTAGE pages ahead: 8 warps x 3 x 8 KiB = 192 KiB in flight per SM;
+//  * each warp keeps its own ring of 4 KiB page slots (K page, V page, ...)
+//    filled by 1-D TMA bulk copies (cp.async.bulk, mbarrier complete_tx) issued
+//    by one lane ahead of the consumer: 16 warps x 3 x 4 KiB = 192 KiB per SM;
 //  * consumer: a 16-token page is read from smem by TPG = head_dim/8 lanes per
-//    token row (16-B vectors, conflict-free), q.k partials reduced with xor
-//    shuffles, online softmax in base 2 (scale*log2 e folded into q), one
-//    rescale per page;
+//    token row (16-B vectors, conflict-free); the q.k partials are
+//    transpose-reduced so every lane ends with ONE token's score (one exp per
+//    token, not per lane), the page max/sum are warp reductions, the running
+//    (m, l) is warp-uniform with a lazy rescale, and each token's weight is
+//    shuffled back to the lanes that hold its V row; full pages take a
+//    mask-free path, only the page holding position c is masked;
 //  * a warp's range covers whole (seq, head) pairs — written straight to `out`
 //    — plus at most a partial first and a partial last pair, whose (m, l, o)
 //    go to the workspace and are merged by decode_combine_kernel (a8);
@@ -29,19 +32,18 @@ namespace ds {
 
 namespace {
 
-constexpr int kWarps = 8;
+constexpr int kWarps = 16;
 constexpr int kMaxSeqs = kDecodeMaxSeqs;
 constexpr float kNegInf = -__builtin_huge_valf();
 
 template <int D>
 struct DecCfg {
-  static constexpr int kPageBytes = 16 * D * 2;
-  static constexpr int kStageBytes = 2 * kPageBytes;  // K page + V page
-  static constexpr int kStages = D == 128 ? 3 : 6;
-  static constexpr int kRingBytes = kWarps * kStages * kStageBytes;
-  static constexpr int kPrefixOff = kRingBytes;  // int[kMaxSeqs + 1]
+  static constexpr int kPageBytes = 16 * D * 2;         // one K or V page of one head
+  static constexpr int kSlots = D == 128 ? 3 : 6;        // half-stages in flight per warp
+  static constexpr int kRingBytes = kWarps * kSlots * kPageBytes;
+  static constexpr int kPrefixOff = kRingBytes;          // int[kMaxSeqs + 1]
   static constexpr int kBarOff = (kPrefixOff + (kMaxSeqs + 1) * 4 + 7) & ~7;
-  static constexpr int kSmem = kBarOff + kWarps * kStages * 8;
+  static constexpr int kSmem = kBarOff + kWarps * kSlots * 8;
 };
 
 DS_DEVICE float dot8(const float (&q)[8], const uint4 &k) {
@@ -130,17 +132,80 @@ DS_DEVICE void advance(PagePos &q, const int *prefix, int n) {
   }
 }
 
+// One page of 16 tokens for one warp. Lane (g, dpart): token rows t = it*GPW + g,
+// dims [8*dpart, 8*dpart+8). kLast: the page holding position c (masked; token c
+// comes from k_new/v_new).
+template <int D, bool kLast>
+DS_DEVICE void consume_page(const uint8_t *kst, const uint8_t *vst, const float (&q)[8], float (&acc)[8],
+                            float &m, float &l, int lane, int pos0, int c, const uint16_t *knew,
+                            const uint16_t *vnew) {
+  constexpr int TPG = D / 8, GPW = 32 / TPG, NIT = 16 / GPW;  // NIT == TPG / 2
+  const int g = lane / TPG, dpart = lane % TPG;
+  // q.k partial sums of this lane's NIT rows
+  float v[NIT];
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int t = it * GPW + g;
+    uint4 kk = *reinterpret_cast<const uint4 *>(kst + t * (D * 2) + dpart * 16);
+    if (kLast && pos0 + t == c) kk = *reinterpret_cast<const uint4 *>(knew);
+    v[it] = dot8(q, kk);
+  }
+  // transpose-reduce over the TPG lanes: afterwards lane holds the full score of
+  // row r = (lane >> 1) & (NIT - 1) (lanes 2k and 2k+1 hold the same row)
+  int cnt = NIT;
+#pragma unroll
+  for (int o = TPG / 2; o >= 2; o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int j = 0; j < NIT / 2; ++j) {
+      if (j < cnt / 2) {
+        const float send = up ? v[j] : v[j + cnt / 2];
+        const float keep = up ? v[j + cnt / 2] : v[j];
+        v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    }
+    cnt >>= 1;
+  }
+  float s = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+  const int my_t = ((lane >> 1) & (NIT - 1)) * GPW + g;
+  if (kLast && pos0 + my_t > c) s = kNegInf;
+  // warp max / sum over the 16 distinct scores (skip xor 1: duplicates)
+  float pmax = s;
+#pragma unroll
+  for (int o = 2; o < 32; o <<= 1) pmax = fmaxf(pmax, __shfl_xor_sync(0xffffffffu, pmax, o));
+  const float m_new = fmaxf(m, pmax);  // finite: every page has >= 1 valid token
+  const float p = ex2(s - m_new);
+  float psum = p;
+#pragma unroll
+  for (int o = 2; o < 32; o <<= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
+  if (m_new != m) {  // warp-uniform; lazy rescale
+    const float alpha = rescale(m, m_new);
+    l *= alpha;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= alpha;
+    m = m_new;
+  }
+  l += psum;
+  // P.V: broadcast the weight of each of this lane's rows from its owner lane
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int t = it * GPW + g;
+    const float pw = __shfl_sync(0xffffffffu, p, g * TPG + it * 2);
+    uint4 vv = *reinterpret_cast<const uint4 *>(vst + t * (D * 2) + dpart * 16);
+    if (kLast && pos0 + t == c) vv = *reinterpret_cast<const uint4 *>(vnew);
+    axpy8(acc, pw, vv);
+  }
+}
+
 template <int D>
 __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs a) {
   using C = DecCfg<D>;
-  constexpr int TPG = D / 8;     // lanes per token row
-  constexpr int GPW = 32 / TPG;  // token rows per warp instruction
-  constexpr int NIT = 16 / GPW;  // rows per lane per page
+  constexpr int TPG = D / 8;  // lanes per token row
   extern __shared__ __align__(128) uint8_t smem[];
   int *prefix = reinterpret_cast<int *>(smem + C::kPrefixOff);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + C::kBarOff);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane / TPG, dpart = lane % TPG;
+  const int dpart = lane % TPG;
   const int B = a.num_seqs, n = a.n_loc;
 
   build_prefix(a.cache_lens, B, prefix);
@@ -153,10 +218,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   const int64_t x0 = range_begin(gw, W, P), x1 = range_begin(gw + 1, W, P);
   if (x0 >= x1) return;
 
-  uint8_t *ring = smem + warp * C::kStages * C::kStageBytes;
-  uint64_t *wbar = bars + warp * C::kStages;
+  // per-warp ring of kSlots half-stages: slot 2k holds a K page, 2k+1 its V page
+  uint8_t *ring = smem + warp * C::kSlots * C::kPageBytes;
+  uint64_t *wbar = bars + warp * C::kSlots;
   if (lane == 0) {
-    for (int s = 0; s < C::kStages; ++s) mbar_init(&wbar[s], 1);
+    for (int s = 0; s < C::kSlots; ++s) mbar_init(&wbar[s], 1);
     fence_barrier_init();
   }
   __syncwarp();
@@ -165,21 +231,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   const size_t kv_stride = (size_t)a.num_blocks * n * page_elems;  // K -> V
   const uint16_t *layer_base = a.cache + (size_t)a.layer * 2 * kv_stride;
 
-  // producer (lane 0): TMA bulk copies NSTAGE pages ahead of the consumer
+  // producer (lane 0): TMA bulk copies of K/V pages, kSlots half-pages ahead
   PagePos pq = locate(x0, prefix, B, n);
-  int64_t issued = x0;
-  auto issue = [&](int stage) {
-    const int blk = a.block_table[(size_t)pq.b * a.max_blocks + pq.p];
-    const uint16_t *kp = layer_base + ((size_t)blk * n + pq.h) * page_elems;
-    uint8_t *dst = ring + stage * C::kStageBytes;
-    mbar_arrive_expect_tx(&wbar[stage], C::kStageBytes);
-    bulk_g2s(dst, kp, C::kPageBytes, &wbar[stage]);
-    bulk_g2s(dst + C::kPageBytes, kp + kv_stride, C::kPageBytes, &wbar[stage]);
-    advance(pq, prefix, n);
-    ++issued;
+  const int64_t h_end = 2 * (x1 - x0);  // half-pages of this warp
+  int64_t h_issued = 0;
+  const uint16_t *cur_page = nullptr;
+  auto issue = [&]() {
+    const int slot = (int)(h_issued % C::kSlots);
+    if ((h_issued & 1) == 0) {
+      const int blk = a.block_table[(size_t)pq.b * a.max_blocks + pq.p];
+      cur_page = layer_base + ((size_t)blk * n + pq.h) * page_elems;
+      advance(pq, prefix, n);
+    }
+    mbar_arrive_expect_tx(&wbar[slot], C::kPageBytes);
+    bulk_g2s(ring + slot * C::kPageBytes, cur_page + ((h_issued & 1) ? kv_stride : 0), C::kPageBytes,
+             &wbar[slot]);
+    ++h_issued;
   };
   if (lane == 0)
-    for (int s = 0; s < C::kStages && issued < x1; ++s) issue(s);
+    while (h_issued < h_end && h_issued < C::kSlots) issue();
 
   // consumer
   PagePos cq = locate(x0, prefix, B, n);
@@ -187,8 +257,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   bool first_seg = true;
   float q[8], m = kNegInf, l = 0.f, acc[8];
   int c = 0;
+  size_t row = 0;
   auto load_pair = [&]() {
-    const size_t row = ((size_t)cq.b * n + cq.h) * D + dpart * 8;
+    row = ((size_t)cq.b * n + cq.h) * D + dpart * 8;
     const uint4 qv = *reinterpret_cast<const uint4 *>(a.q + row);
     const float s = a.scale_log2;
     q[0] = bf16lo(qv.x) * s; q[1] = bf16hi(qv.x) * s;
@@ -204,80 +275,37 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   load_pair();
 
   for (int64_t x = x0; x < x1; ++x) {
-    const int it_idx = (int)(x - x0);
-    const int stage = it_idx % C::kStages;
-    const size_t row = ((size_t)cq.b * n + cq.h) * D + dpart * 8;
-    // (i) fused append: the owner of the page holding position c stores the new token
-    if (cq.p == (c >> 4) && lane < 2 * TPG) {
+    const int64_t hk = 2 * (x - x0);
+    const int sk = (int)(hk % C::kSlots), sv = (int)((hk + 1) % C::kSlots);
+    const bool last = cq.p == (c >> 4);
+    if (last && lane < 2 * TPG) {  // (i) fused append of the new token at position c
       const int kv = lane / TPG;
-      const size_t r2 = ((size_t)cq.b * n + cq.h) * D + (lane % TPG) * 8;
       const int blk = a.block_table[(size_t)cq.b * a.max_blocks + cq.p];
       uint16_t *dst = const_cast<uint16_t *>(layer_base) + kv * kv_stride +
                       ((size_t)blk * n + cq.h) * page_elems + (size_t)(c & 15) * D + (lane % TPG) * 8;
+      const size_t r2 = ((size_t)cq.b * n + cq.h) * D + (lane % TPG) * 8;
       *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>((kv ? a.v_new : a.k_new) + r2);
     }
-    mbar_wait(&wbar[stage], (it_idx / C::kStages) & 1);
-    const uint8_t *kst = ring + stage * C::kStageBytes;
-    const uint8_t *vst = kst + C::kPageBytes;
-    uint4 kr[NIT], vr[NIT];
-#pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-      const int t = it * GPW + g;
-      const bool is_new = cq.p * 16 + t == c;
-      kr[it] = is_new ? *reinterpret_cast<const uint4 *>(a.k_new + row)
-                      : *reinterpret_cast<const uint4 *>(kst + t * (D * 2) + dpart * 16);
-      vr[it] = is_new ? *reinterpret_cast<const uint4 *>(a.v_new + row)
-                      : *reinterpret_cast<const uint4 *>(vst + t * (D * 2) + dpart * 16);
-    }
-    // the stage is consumed (values are in registers): refill it NSTAGE pages ahead
+    mbar_wait(&wbar[sk], (int)((hk / C::kSlots) & 1));
+    mbar_wait(&wbar[sv], (int)(((hk + 1) / C::kSlots) & 1));
+    const uint8_t *kst = ring + sk * C::kPageBytes, *vst = ring + sv * C::kPageBytes;
+    if (last)
+      consume_page<D, true>(kst, vst, q, acc, m, l, lane, cq.p * 16, c, a.k_new + row, a.v_new + row);
+    else
+      consume_page<D, false>(kst, vst, q, acc, m, l, lane, cq.p * 16, c, nullptr, nullptr);
+    // both half-stages consumed: refill them kSlots half-pages ahead
     __syncwarp();
-    if (lane == 0 && issued < x1) {
+    if (lane == 0 && h_issued < h_end) {
       fence_proxy_async_smem();
-      issue(stage);
+      issue();
+      if (h_issued < h_end) issue();
     }
-    float s[NIT];
-    float pmax = kNegInf;
-#pragma unroll
-    for (int it = 0; it < NIT; ++it) {
-      float xv = dot8(q, kr[it]);
-#pragma unroll
-      for (int off = TPG / 2; off >= 1; off >>= 1) xv += __shfl_xor_sync(0xffffffffu, xv, off);
-      s[it] = (cq.p * 16 + it * GPW + g) <= c ? xv : kNegInf;
-      pmax = fmaxf(pmax, s[it]);
-    }
-    const float m_new = fmaxf(m, pmax);
-    if (m_new != kNegInf) {
-      const float alpha = rescale(m, m_new);
-      l *= alpha;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) acc[e] *= alpha;
-#pragma unroll
-      for (int it = 0; it < NIT; ++it) {
-        if (s[it] != kNegInf) {
-          const float pr = ex2(s[it] - m_new);
-          l += pr;
-          axpy8(acc, pr, vr[it]);
-        }
-      }
-      m = m_new;
-    }
-    // end of a segment: this pair's pages inside our range are done
     const bool pair_end = cq.p == cq.npg - 1;
     if (pair_end || x == x1 - 1) {
 #pragma unroll
-      for (int off = TPG; off < 32; off <<= 1) {  // merge the GPW token-row groups
-        const float mo = __shfl_xor_sync(0xffffffffu, m, off);
-        const float lo = __shfl_xor_sync(0xffffffffu, l, off);
-        const float mm = fmaxf(m, mo);
-        const float wa = rescale(m, mm), wb = rescale(mo, mm);
-        l = l * wa + lo * wb;
+      for (int off = TPG; off < 32; off <<= 1)  // sum the token-row groups (same m)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float ao = __shfl_xor_sync(0xffffffffu, acc[e], off);
-          acc[e] = acc[e] * wa + ao * wb;
-        }
-        m = mm;
-      }
+        for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], off);
       if (seg_begin == 0 && pair_end) {  // the whole pair is ours: final output
         if (lane < TPG) {
           const float inv = 1.f / l;
@@ -335,13 +363,15 @@ __global__ void __launch_bounds__(128) decode_combine_kernel(const DecodeArgs a,
   if (w0 == w1) return;  // written directly by its warp
   constexpr int PER = D / 32;
   const int slot0 = range_begin(w0, W, P) < start ? 1 : 0;  // pair is w0's last segment
+  auto empty = [&](int64_t w) { return range_begin(w, W, P) == range_begin(w + 1, W, P); };
   float mm = kNegInf;
   for (int64_t w = w0; w <= w1; ++w)
-    mm = fmaxf(mm, a.workspace[((size_t)w * 2 + (w == w0 ? slot0 : 0)) * (D + 2) + D]);
+    if (!empty(w)) mm = fmaxf(mm, a.workspace[((size_t)w * 2 + (w == w0 ? slot0 : 0)) * (D + 2) + D]);
   float lt = 0.f, ot[PER];
 #pragma unroll
   for (int e = 0; e < PER; ++e) ot[e] = 0.f;
   for (int64_t w = w0; w <= w1; ++w) {
+    if (empty(w)) continue;
     const float *ws = a.workspace + ((size_t)w * 2 + (w == w0 ? slot0 : 0)) * (D + 2);
     const float wt = rescale(ws[D], mm);
     lt += ws[D + 1] * wt;
