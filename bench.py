@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--profile", action="store_true", help="one short pass for ncu (no JSON)")
+    p.add_argument("--no-graphs", action="store_true", help="eager decode launches (no CUDA graphs)")
     return p.parse_args()
 
 
@@ -172,9 +173,17 @@ class Engine:
             self.dk = torch.randn(dshape, generator=g, device=dev, dtype=torch.float32).to(bf)
             self.dv = torch.randn(dshape, generator=g, device=dev, dtype=torch.float32).to(bf)
             self.dout = torch.empty((w.out_len, w.B, w.n, w.d), dtype=bf, device=dev)
-            max_c = w.l0 + w.out_len
-            self.ws = torch.empty(max(16, ds.ds_decode_workspace_bytes(w.B, w.n, w.d, max_c)), dtype=torch.uint8,
-                                  device=dev)
+            self.max_c = w.l0 + w.out_len - 1  # largest cache length of the batch (validation only)
+            self.ws = torch.empty(max(16, ds.ds_decode_workspace_bytes(w.B, w.n, w.d, self.max_c)),
+                                  dtype=torch.uint8, device=dev)
+            # fixed device block table / lengths read by the captured decode graphs
+            self.dtab = torch.full((w.B, w.maxb), -1, dtype=torch.int32, device=dev)
+            self.dlen = torch.zeros((w.B,), dtype=torch.int32, device=dev)
+            self.h_tab2 = [torch.empty((w.B, w.maxb), dtype=torch.int32).pin_memory() for _ in range(2)]
+            self.h_len2 = [torch.empty((w.B,), dtype=torch.int32).pin_memory() for _ in range(2)]
+            self.h_ev2 = [None, None]
+            self.hslot = 0
+            self.graphs = None
         nblk = w.B * w.pages_per_seq
         mrole = {"both": ds.DS_MIGRATE_LOCAL, "prefill": ds.DS_MIGRATE_SEND, "decode": ds.DS_MIGRATE_RECV}[role]
         self.mrole = mrole
@@ -192,6 +201,38 @@ class Engine:
         self.stream = torch.cuda.current_stream()
         self.launches = 0
         self.decode_events = []
+
+    def upload_fixed(self, table: np.ndarray, lens):
+        """async H2D of the decode block table + lengths into the graphs' fixed buffers"""
+        i = self.hslot
+        self.hslot ^= 1
+        if self.h_ev2[i] is not None:
+            self.h_ev2[i].synchronize()
+        self.h_tab2[i].numpy()[:] = table
+        self.h_len2[i].numpy()[:] = lens
+        self.dtab.copy_(self.h_tab2[i], non_blocking=True)
+        self.dlen.copy_(self.h_len2[i], non_blocking=True)
+        ev = self.torch.cuda.Event()
+        ev.record()
+        self.h_ev2[i] = ev
+
+    def decode_layers(self, s):
+        """ds_decode_attn for every layer of decode step s (reads dtab / dlen)"""
+        w, ds = self.w, self.ds
+        for layer in range(w.L):
+            ds.ds_decode_attn(self.dq[s, layer], self.dk[s, layer], self.dv[s, layer], self.dout[s], self.D, layer,
+                              self.dtab, self.dlen, self.max_c, w.scale, self.ws)
+
+    def capture_decode_graphs(self):
+        """one CUDA graph per decode step: the 40-layer loop becomes a single launch"""
+        torch = self.torch
+        self.graphs = []
+        for s in range(self.w.out_len):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self.decode_layers(s)
+            self.graphs.append(g)
+        torch.cuda.synchronize()
 
     def upload(self, table: np.ndarray, lens):
         """async H2D of a block table (+ lengths) through the pinned ring"""
@@ -251,17 +292,12 @@ class Engine:
             cur = list(w.lens)
             for s in range(w.out_len):
                 ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, cur, [1] * w.B, td)
-                td_d, cl = self.upload(td, cur)
-                for layer in range(w.L):
-                    if time_decode:
-                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                        e0.record()
-                    ds.ds_decode_attn(self.dq[s, layer], self.dk[s, layer], self.dv[s, layer], self.dout[s], self.D,
-                                      layer, td_d, cl, max(cur), w.scale, self.ws)
-                    if time_decode:
-                        e1.record()
-                        self.decode_events.append((e0, e1, list(cur)))
-                self.launches += 2 * w.L  # decode_kernel + decode_combine_kernel
+                self.upload_fixed(td, cur)
+                if self.graphs is not None:
+                    self.graphs[s].replay()
+                else:
+                    self.decode_layers(s)
+                self.launches += 2 * w.L  # decode_kernel + decode_combine_kernel per layer
                 cur = [c + 1 for c in cur]
             ds.ds_block_table(self.pool_d, ds.DS_BT_FREE, cur, None, td)
         if "end" in ev:
@@ -389,6 +425,10 @@ def run_ds(args):
     for _ in range(args.warmup):
         eng.step()
     torch.cuda.synchronize()
+    if eng.dc and not args.no_graphs:
+        eng.capture_decode_graphs()
+        eng.step()  # one graph-replay warm-up step
+        torch.cuda.synchronize()
     barrier(world)
     sampler = ClockSampler(local)
     sampler.start()
@@ -402,7 +442,7 @@ def run_ds(args):
     t_start.record()
     for s in range(args.steps):
         evs = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "prefill_end", "migrate_end", "end")}
-        eng.step(evs, time_decode=True)
+        eng.step(evs)
         phase.append(evs)
     t_end.record()
     torch.cuda.synchronize()
@@ -437,20 +477,18 @@ def run_ds(args):
         dec_ms = statistics.median(e["migrate_end"].elapsed_time(e["end"]) for e in phase)
         comp["decode_ms_per_step"] = dec_ms
         comp["decode_tok_s_per_gpu"] = w.B * w.out_len / (dec_ms / 1e3)
-        times, nbytes = [], []
-        for (e0, e1, cur) in eng.decode_events:
-            times.append(e0.elapsed_time(e1))
-            nbytes.append(w.decode_bytes(cur))
-        avg_ms = sum(times) / len(times)
-        avg_bytes = sum(nbytes) / len(nbytes)
+        ctx_steps = [[c + s for c in w.lens] for s in range(w.out_len)]
+        avg_bytes = sum(w.decode_bytes(c) for c in ctx_steps) / w.out_len
+        avg_ms = dec_ms / (w.out_len * w.L)  # device time per ds_decode_attn call (both kernels + gaps)
         dec_kernel = (avg_bytes, avg_ms)
         comp["decode_attn_GBps"] = avg_bytes / (avg_ms / 1e3) / 1e9
         comp["decode_attn_frac_of_hbm"] = comp["decode_attn_GBps"] / peaks["hbm_gbs"]
         comp["decode_attn_us_per_launch"] = avg_ms * 1e3
+        comp["decode_graphs"] = eng.graphs is not None
     roofline = None
     if dec_kernel:
         achieved = dec_kernel[0] / (dec_kernel[1] / 1e3) / 1e9
-        roofline = {"kernel": "ds_decode_attn (decode_split_kernel)", "bound": "hbm", "achieved": achieved,
+        roofline = {"kernel": "ds_decode_attn (decode_kernel + decode_combine_kernel)", "bound": "hbm", "achieved": achieved,
                     "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
                     "traffic": None, "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                     "algorithmic_bytes_per_launch": dec_kernel[0]}

@@ -393,21 +393,24 @@ size_t decode_workspace_bytes(int num_seqs, int head_dim, int num_sms) {
 
 int decode_warps_per_cta() { return kWarps; }
 
+template <int D>
+static cudaError_t set_decode_smem_once() {
+  static cudaError_t st = cudaFuncSetAttribute(decode_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               DecCfg<D>::kSmem);  // thread-safe static init, once
+  return st;
+}
+
 cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaStream_t stream) {
   const int warps_total = num_sms * kWarps;
   const int combine_blocks = (a.num_seqs * a.n_loc + 3) / 4;
   cudaError_t e;
   if (head_dim == 128) {
-    const int smem = DecCfg<128>::kSmem;
-    e = cudaFuncSetAttribute(decode_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    decode_kernel<128><<<num_sms, kWarps * 32, smem, stream>>>(a);
+    if ((e = set_decode_smem_once<128>()) != cudaSuccess) return e;
+    decode_kernel<128><<<num_sms, kWarps * 32, DecCfg<128>::kSmem, stream>>>(a);
     decode_combine_kernel<128><<<combine_blocks, 128, 0, stream>>>(a, warps_total);
   } else {
-    const int smem = DecCfg<64>::kSmem;
-    e = cudaFuncSetAttribute(decode_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    decode_kernel<64><<<num_sms, kWarps * 32, smem, stream>>>(a);
+    if ((e = set_decode_smem_once<64>()) != cudaSuccess) return e;
+    decode_kernel<64><<<num_sms, kWarps * 32, DecCfg<64>::kSmem, stream>>>(a);
     decode_combine_kernel<64><<<combine_blocks, 128, 0, stream>>>(a, warps_total);
   }
   return cudaGetLastError();

@@ -287,6 +287,13 @@ size_t prefill_smem_bytes(int head_dim) {
   return head_dim == 128 ? Smem<128>::ALLOC : Smem<64>::ALLOC;
 }
 
+template <int D>
+static cudaError_t set_prefill_smem_once() {
+  static cudaError_t st = cudaFuncSetAttribute(prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)Smem<D>::ALLOC);
+  return st;
+}
+
 cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
                            const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
                            cudaStream_t stream) {
@@ -294,12 +301,10 @@ cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const 
   const size_t smem = prefill_smem_bytes(head_dim);
   cudaError_t e;
   if (head_dim == 128) {
-    e = cudaFuncSetAttribute(prefill_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    if ((e = set_prefill_smem_once<128>()) != cudaSuccess) return e;
     prefill_kernel<128><<<grid, kThreads, smem, stream>>>(tm_q, tm_k, tm_v, tm_cache, a);
   } else {
-    e = cudaFuncSetAttribute(prefill_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    if ((e = set_prefill_smem_once<64>()) != cudaSuccess) return e;
     prefill_kernel<64><<<grid, kThreads, smem, stream>>>(tm_q, tm_k, tm_v, tm_cache, a);
   }
   return cudaGetLastError();
