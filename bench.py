@@ -174,7 +174,7 @@ class Engine:
             self.dv = torch.randn(dshape, generator=g, device=dev, dtype=torch.float32).to(bf)
             self.dout = torch.empty((w.out_len, w.B, w.n, w.d), dtype=bf, device=dev)
             self.max_c = w.l0 + w.out_len - 1  # largest cache length of the batch (validation only)
-            self.ws = torch.empty(max(16, ds.ds_decode_workspace_bytes(w.B, w.n, w.d, self.max_c)),
+            self.ws = torch.zeros(max(16, ds.ds_decode_workspace_bytes(w.B, w.n, w.d, self.max_c)),
                                   dtype=torch.uint8, device=dev)
             # fixed device block table / lengths read by the captured decode graphs
             self.dtab = torch.full((w.B, w.maxb), -1, dtype=torch.int32, device=dev)

@@ -151,8 +151,13 @@ ds_status ds_prefill_attn(const void *q, const void *k, const void *v, void *out
  * cache_lens  : device int32 [num_seqs], c >= 0; max_cache_len >= every c
  *               (host value; sizes the split-K grid).
  * workspace   : device scratch of >= ds_decode_workspace_bytes(...) bytes, 16-B
- *               aligned, caller-owned, contents need no initialisation.
- * The split-K partials (m, l, o) are merged with a log-sum-exp combine (a8).
+ *               aligned, caller-owned. It must be ZEROED once before its first
+ *               use (e.g. torch.zeros); every call leaves it zeroed again (it
+ *               holds split partials and self-resetting merge tickets). Calls
+ *               sharing a workspace must be ordered on one stream.
+ * Work split: the (seq, head, page) space is cut into equal page ranges, one
+ * per warp of a persistent grid; a pair that straddles ranges is merged from
+ * its partials (m, l, o) with the log-sum-exp rule (a8), inside the same launch.
  * Errors: DS_ERR_INVALID_ARG, DS_ERR_CUDA. */
 size_t ds_decode_workspace_bytes(int32_t num_seqs, int32_t n_loc, int32_t head_dim,
                                  int32_t max_cache_len);

@@ -119,10 +119,6 @@ static int device_sms() {
     return sms < kDecodeMaxSMs ? sms : kDecodeMaxSMs;
   return 148;
 }
-// workspace = [kDecodeMaxSMs * warps][2][D+2] floats, then the int32 page prefix [B+1]
-static size_t decode_partials_bytes(int head_dim) {
-  return decode_workspace_bytes(0, head_dim, kDecodeMaxSMs) - 4 - 64;
-}
 
 }  // namespace ds
 
@@ -177,7 +173,7 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
 extern "C" size_t ds_decode_workspace_bytes(int32_t num_seqs, int32_t n_loc, int32_t head_dim,
                                             int32_t max_cache_len) {
   if (num_seqs <= 0 || n_loc <= 0 || (head_dim != 64 && head_dim != 128) || max_cache_len < 0) return 0;
-  return decode_workspace_bytes(num_seqs, head_dim, kDecodeMaxSMs);
+  return decode_workspace_bytes(num_seqs, n_loc, head_dim, kDecodeMaxSMs);
 }
 
 extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void *v_new, void *out,
@@ -215,7 +211,7 @@ extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void
   a.block_table = block_table;
   a.cache_lens = cache_lens;
   a.workspace = static_cast<float *>(workspace);
-  a.ws_prefix = reinterpret_cast<int32_t *>(static_cast<char *>(workspace) + decode_partials_bytes(D));
+  a.tickets = reinterpret_cast<int32_t *>(static_cast<char *>(workspace) + decode_partials_bytes(D, kDecodeMaxSMs));
   a.layer = layer;
   a.num_blocks = cache->num_blocks;
   a.n_loc = n;

@@ -22,7 +22,10 @@
 //    mask-free path, only the page holding position c is masked;
 //  * a warp's range covers whole (seq, head) pairs — written straight to `out`
 //    — plus at most a partial first and a partial last pair, whose (m, l, o)
-//    go to the workspace and are merged by decode_combine_kernel (a8);
+//    go to the workspace; the warp that publishes a pair's last partial merges
+//    them (a8, fused; atomic ticket per pair, self-resetting);
+//  * launched with programmatic dependent launch (griddepcontrol.wait before
+//    the first read), so launch latency overlaps the previous kernel's tail;
 //  * the append (i) is fused: the warp that owns the page holding position c
 //    stores k_new/v_new into it and uses them from global memory for token c.
 #include "common.cuh"
@@ -132,6 +135,64 @@ DS_DEVICE void advance(PagePos &q, const int *prefix, int n) {
   }
 }
 
+// owner warp of flattened page x: B_w <= x < B_{w+1}
+DS_DEVICE int64_t owner_of(int64_t x, int64_t W, int64_t P) {
+  int64_t w = x * W / P;
+  while (w + 1 < W && range_begin(w + 1, W, P) <= x) ++w;
+  while (w > 0 && range_begin(w, W, P) > x) --w;
+  return w;
+}
+
+// a8, fused: the warp that publishes the LAST partial of a straddling (seq, head)
+// pair merges all of them (log-sum-exp rule) and resets the pair's ticket:
+//   m* = max_k m_k ; l* = sum_k l_k 2^(m_k - m*) ; o = sum_k o_k 2^(m_k - m*) / l*
+// Partials are published with a release fence + atomic ticket; the merger reads
+// them with an acquire fence through L2 (ld.cg).
+template <int D>
+DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int h, int64_t W, int64_t P,
+                             int lane) {
+  const int n = a.n_loc;
+  const int npg = prefix[b + 1] - prefix[b];
+  const int64_t start = (int64_t)n * prefix[b] + (int64_t)h * npg;
+  const int64_t w0 = owner_of(start, W, P), w1 = owner_of(start + npg - 1, W, P);
+  int need = 0;
+  for (int64_t w = w0; w <= w1; ++w) need += range_begin(w, W, P) < range_begin(w + 1, W, P);
+  __syncwarp();
+  int ticket = 0;
+  const int pair = b * n + h;
+  if (lane == 0) {
+    __threadfence();
+    ticket = atomicAdd(&a.tickets[pair], 1);
+  }
+  ticket = __shfl_sync(0xffffffffu, ticket, 0);
+  if (ticket != need - 1) return;
+  __threadfence();
+  const int slot0 = range_begin(w0, W, P) < start ? 1 : 0;  // the pair is w0's last segment
+  constexpr int PER = D / 32;
+  float mm = kNegInf;
+  for (int64_t w = w0; w <= w1; ++w) {
+    if (range_begin(w, W, P) == range_begin(w + 1, W, P)) continue;
+    mm = fmaxf(mm, __ldcg(a.workspace + ((size_t)w * 2 + (w == w0 ? slot0 : 0)) * (D + 2) + D));
+  }
+  float lt = 0.f, ot[PER];
+#pragma unroll
+  for (int e = 0; e < PER; ++e) ot[e] = 0.f;
+  for (int64_t w = w0; w <= w1; ++w) {
+    if (range_begin(w, W, P) == range_begin(w + 1, W, P)) continue;
+    const float *ws = a.workspace + ((size_t)w * 2 + (w == w0 ? slot0 : 0)) * (D + 2);
+    const float wt = rescale(__ldcg(ws + D), mm);
+    lt += __ldcg(ws + D + 1) * wt;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) ot[e] += __ldcg(ws + lane * PER + e) * wt;
+  }
+  const float inv = 1.f / lt;
+  uint16_t *o = reinterpret_cast<uint16_t *>(a.out) + ((size_t)b * n + h) * D + lane * PER;
+#pragma unroll
+  for (int e = 0; e < PER; e += 2)
+    *reinterpret_cast<uint32_t *>(o + e) = pack_bf16(ot[e] * inv, ot[e + 1] * inv);
+  if (lane == 0) a.tickets[pair] = 0;  // self-cleaning: the workspace stays ready
+}
+
 // One page of 16 tokens for one warp. Lane (g, dpart): token rows t = it*GPW + g,
 // dims [8*dpart, 8*dpart+8). kLast: the page holding position c (masked; token c
 // comes from k_new/v_new).
@@ -208,10 +269,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   const int dpart = lane % TPG;
   const int B = a.num_seqs, n = a.n_loc;
 
+  // PDL: the launch and CTA set-up overlap the previous kernel's tail; nothing
+  // written by an earlier kernel (lengths, tables, pages, workspace) is read
+  // before this wait.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   build_prefix(a.cache_lens, B, prefix);
-  if (blockIdx.x == 0) {  // publish the plan for the combine kernel
-    for (int b = threadIdx.x; b <= B; b += blockDim.x) a.ws_prefix[b] = prefix[b];
-  }
   const int64_t P = (int64_t)n * prefix[B];
   const int64_t W = (int64_t)gridDim.x * kWarps;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
@@ -316,7 +378,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
           o.w = pack_bf16(acc[6] * inv, acc[7] * inv);
           *reinterpret_cast<uint4 *>(reinterpret_cast<uint16_t *>(a.out) + row) = o;
         }
-      } else {  // a straddling pair: partial (o, m, l) for the combine
+      } else {  // a straddling pair: partial (o, m, l), merged by the last contributor (a8)
         float *ws = a.workspace + ((size_t)gw * 2 + (first_seg ? 0 : 1)) * (D + 2);
         if (lane < TPG) {
 #pragma unroll
@@ -326,6 +388,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
             ws[D + 1] = l;
           }
         }
+        merge_if_last<D>(a, prefix, cq.b, cq.h, W, P, lane);
       }
       first_seg = false;
       if (x + 1 < x1) {
@@ -339,56 +402,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   }
 }
 
-// a8: merge the partials of the pairs that straddle warp ranges:
-//   m* = max_k m_k ; l* = sum_k l_k 2^(m_k - m*) ; o = sum_k o_k 2^(m_k - m*) / l*
-template <int D>
-__global__ void __launch_bounds__(128) decode_combine_kernel(const DecodeArgs a, int warps_total) {
-  const int n = a.n_loc, B = a.num_seqs;
-  const int pair = blockIdx.x * 4 + (threadIdx.x >> 5);
-  if (pair >= B * n) return;
-  const int lane = threadIdx.x & 31;
-  const int b = pair / n, h = pair % n;
-  const int *prefix = a.ws_prefix;
-  const int64_t P = (int64_t)n * prefix[B];
-  const int npg = prefix[b + 1] - prefix[b];
-  const int64_t start = (int64_t)n * prefix[b] + (int64_t)h * npg, last = start + npg - 1;
-  const int64_t W = warps_total;
-  auto owner = [&](int64_t x) {
-    int64_t w = x * W / P;
-    while (w + 1 < W && range_begin(w + 1, W, P) <= x) ++w;
-    while (w > 0 && range_begin(w, W, P) > x) --w;
-    return w;
-  };
-  const int64_t w0 = owner(start), w1 = owner(last);
-  if (w0 == w1) return;  // written directly by its warp
-  constexpr int PER = D / 32;
-  const int slot0 = range_begin(w0, W, P) < start ? 1 : 0;  // pair is w0's last segment
-  auto empty = [&](int64_t w) { return range_begin(w, W, P) == range_begin(w + 1, W, P); };
-  float mm = kNegInf;
-  for (int64_t w = w0; w <= w1; ++w)
-    if (!empty(w)) mm = fmaxf(mm, a.workspace[((size_t)w * 2 + (w == w0 ? slot0 : 0)) * (D + 2) + D]);
-  float lt = 0.f, ot[PER];
-#pragma unroll
-  for (int e = 0; e < PER; ++e) ot[e] = 0.f;
-  for (int64_t w = w0; w <= w1; ++w) {
-    if (empty(w)) continue;
-    const float *ws = a.workspace + ((size_t)w * 2 + (w == w0 ? slot0 : 0)) * (D + 2);
-    const float wt = rescale(ws[D], mm);
-    lt += ws[D + 1] * wt;
-#pragma unroll
-    for (int e = 0; e < PER; ++e) ot[e] += ws[lane * PER + e] * wt;
-  }
-  const float inv = 1.f / lt;
-  uint16_t *o = reinterpret_cast<uint16_t *>(a.out) + ((size_t)b * n + h) * D + lane * PER;
-#pragma unroll
-  for (int e = 0; e < PER; e += 2)
-    *reinterpret_cast<uint32_t *>(o + e) = pack_bf16(ot[e] * inv, ot[e + 1] * inv);
-}
-
 }  // namespace
 
-size_t decode_workspace_bytes(int num_seqs, int head_dim, int num_sms) {
-  return (size_t)num_sms * kWarps * 2 * (head_dim + 2) * sizeof(float) + (size_t)(num_seqs + 1) * 4 + 64;
+size_t decode_partials_bytes(int head_dim, int num_sms) {
+  return (size_t)num_sms * kWarps * 2 * (head_dim + 2) * sizeof(float);
+}
+size_t decode_workspace_bytes(int num_seqs, int n_loc, int head_dim, int num_sms) {
+  return decode_partials_bytes(head_dim, num_sms) + (size_t)num_seqs * n_loc * 4;  // + tickets
 }
 
 int decode_warps_per_cta() { return kWarps; }
@@ -401,18 +421,26 @@ static cudaError_t set_decode_smem_once() {
 }
 
 cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaStream_t stream) {
-  const int warps_total = num_sms * kWarps;
-  const int combine_blocks = (a.num_seqs * a.n_loc + 3) / 4;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(num_sms);
+  cfg.blockDim = dim3(kWarps * 32);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   cudaError_t e;
   if (head_dim == 128) {
     if ((e = set_decode_smem_once<128>()) != cudaSuccess) return e;
-    decode_kernel<128><<<num_sms, kWarps * 32, DecCfg<128>::kSmem, stream>>>(a);
-    decode_combine_kernel<128><<<combine_blocks, 128, 0, stream>>>(a, warps_total);
+    cfg.dynamicSmemBytes = DecCfg<128>::kSmem;
+    e = cudaLaunchKernelEx(&cfg, decode_kernel<128>, a);
   } else {
     if ((e = set_decode_smem_once<64>()) != cudaSuccess) return e;
-    decode_kernel<64><<<num_sms, kWarps * 32, DecCfg<64>::kSmem, stream>>>(a);
-    decode_combine_kernel<64><<<combine_blocks, 128, 0, stream>>>(a, warps_total);
+    cfg.dynamicSmemBytes = DecCfg<64>::kSmem;
+    e = cudaLaunchKernelEx(&cfg, decode_kernel<64>, a);
   }
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

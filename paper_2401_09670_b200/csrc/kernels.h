@@ -18,11 +18,12 @@ struct DecodeArgs {
   const int32_t *block_table;         // [B][max_blocks]
   const int32_t *cache_lens;          // [B]
   float *workspace;                   // [warps][2][D+2] straddling-pair partials
-  int32_t *ws_prefix;                 // [B+1] page prefix published for the combine
+  int32_t *tickets;                   // [B][n] merge tickets (zero between launches)
   int32_t layer, num_blocks, n_loc, max_blocks, num_seqs;
   float scale_log2;  // softmax_scale * log2(e)
 };
-size_t decode_workspace_bytes(int num_seqs, int head_dim, int num_sms);
+size_t decode_partials_bytes(int head_dim, int num_sms);
+size_t decode_workspace_bytes(int num_seqs, int n_loc, int head_dim, int num_sms);
 cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaStream_t stream);
 
 // a4 / a6: page rows <-> staging

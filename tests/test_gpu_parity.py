@@ -153,13 +153,14 @@ def run_decode(oracle_mod, ctx, n, d, seed=0, steps=1, fragment=0, q_sigma=1.0, 
     cur = list(ctx)
     errs = []
     scale = 1.0 / math.sqrt(d)
+    # one zeroed workspace reused by every step: the merge tickets must self-reset
+    ws = torch.zeros(max(ds.ds_decode_workspace_bytes(B, n, d, max(total)), 16) // 4 + 4,
+                     dtype=torch.float32, device="cuda")
     for s in range(steps):
         side.append(cur, [1] * B, t_ds, t_or)
         db = syn.decode_batch(seed * 100 + s, B, n, d, q_sigma=q_sigma)
         out = torch.full((B, n, d), float("nan"), dtype=torch.bfloat16, device="cuda")
         mcl = max(cur) if max_cache_len is None else max_cache_len
-        ws = torch.empty(max(ds.ds_decode_workspace_bytes(B, n, d, mcl), 16) // 4 + 4,
-                         dtype=torch.float32, device="cuda")
         ds.ds_decode_attn(to_dev(db.q), to_dev(db.k_new), to_dev(db.v_new), out, side.cache, 0, i32(t_ds),
                           i32(cur), mcl, scale, ws)
         torch.cuda.synchronize()
@@ -338,7 +339,7 @@ def test_end_to_end_prefill_migrate_decode(oracle_mod):
         db = syn.decode_batch(500 + s, B, n, d)
         for layer in range(L):
             o = torch.empty((B, n, d), dtype=torch.bfloat16, device="cuda")
-            ws = torch.empty(ds.ds_decode_workspace_bytes(B, n, d, max(cur)) // 4 + 4, dtype=torch.float32,
+            ws = torch.zeros(ds.ds_decode_workspace_bytes(B, n, d, max(cur)) // 4 + 4, dtype=torch.float32,
                              device="cuda")
             ds.ds_decode_attn(to_dev(db.q), to_dev(db.k_new), to_dev(db.v_new), o, D.cache, layer, i32(td),
                               i32(cur), max(cur), scale, ws)
