@@ -155,35 +155,53 @@ DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int 
   const int npg = prefix[b + 1] - prefix[b];
   const int64_t start = (int64_t)n * prefix[b] + (int64_t)h * npg;
   const int64_t w0 = owner_of(start, W, P), w1 = owner_of(start + npg - 1, W, P);
+  const int k = (int)(w1 - w0 + 1);  // candidate contributors (empty ranges skipped)
+  // lane j looks at contributors j, j+32, ...: is it non-empty?
   int need = 0;
-  for (int64_t w = w0; w <= w1; ++w) need += range_begin(w, W, P) < range_begin(w + 1, W, P);
-  __syncwarp();
+  for (int j = lane; j < k; j += 32) need += range_begin(w0 + j, W, P) < range_begin(w0 + j + 1, W, P);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) need += __shfl_xor_sync(0xffffffffu, need, o);
+  __syncwarp();  // the partial written by lanes < TPG is ordered before the release below
   int ticket = 0;
   const int pair = b * n + h;
-  if (lane == 0) {
-    __threadfence();
-    ticket = atomicAdd(&a.tickets[pair], 1);
-  }
+  if (lane == 0)
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(ticket) : "l"(a.tickets + pair) : "memory");
   ticket = __shfl_sync(0xffffffffu, ticket, 0);
   if (ticket != need - 1) return;
-  __threadfence();
+  __syncwarp();
   const int slot0 = range_begin(w0, W, P) < start ? 1 : 0;  // the pair is w0's last segment
   constexpr int PER = D / 32;
-  float mm = kNegInf;
-  for (int64_t w = w0; w <= w1; ++w) {
-    if (range_begin(w, W, P) == range_begin(w + 1, W, P)) continue;
-    mm = fmaxf(mm, __ldcg(a.workspace + ((size_t)w * 2 + (w == w0 ? slot0 : 0)) * (D + 2) + D));
-  }
-  float lt = 0.f, ot[PER];
+  float mm = kNegInf, lt = 0.f, ot[PER];
 #pragma unroll
   for (int e = 0; e < PER; ++e) ot[e] = 0.f;
-  for (int64_t w = w0; w <= w1; ++w) {
-    if (range_begin(w, W, P) == range_begin(w + 1, W, P)) continue;
-    const float *ws = a.workspace + ((size_t)w * 2 + (w == w0 ? slot0 : 0)) * (D + 2);
-    const float wt = rescale(__ldcg(ws + D), mm);
-    lt += __ldcg(ws + D + 1) * wt;
+  for (int j0 = 0; j0 < k; j0 += 32) {  // 32 contributors per round, loads in parallel
+    const int j = j0 + lane;
+    const int64_t w = w0 + j;
+    const bool live = j < k && range_begin(w, W, P) < range_begin(w + 1, W, P);
+    const float *ws = a.workspace + ((size_t)w * 2 + (j == 0 ? slot0 : 0)) * (D + 2);
+    const float mj = live ? __ldcg(ws + D) : kNegInf;
+    const float lj = live ? __ldcg(ws + D + 1) : 0.f;
+    float mr = mj;
 #pragma unroll
-    for (int e = 0; e < PER; ++e) ot[e] += __ldcg(ws + lane * PER + e) * wt;
+    for (int o = 16; o >= 1; o >>= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+    const float m_new = fmaxf(mm, mr);
+    const float alpha = rescale(mm, m_new);
+    float wj = rescale(mj, m_new), lsum = lj * wj;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+    lt = lt * alpha + lsum;
+#pragma unroll
+    for (int e = 0; e < PER; ++e) ot[e] *= alpha;
+    mm = m_new;
+    const int cnt = min(32, k - j0);
+    for (int jj = 0; jj < cnt; ++jj) {  // lane-parallel over dims, loads independent across jj
+      const float wt = __shfl_sync(0xffffffffu, wj, jj);
+      if (wt != 0.f) {
+        const float *wsj = a.workspace + ((size_t)(w0 + j0 + jj) * 2 + (j0 + jj == 0 ? slot0 : 0)) * (D + 2);
+#pragma unroll
+        for (int e = 0; e < PER; ++e) ot[e] = fmaf(__ldcg(wsj + lane * PER + e), wt, ot[e]);
+      }
+    }
   }
   const float inv = 1.f / lt;
   uint16_t *o = reinterpret_cast<uint16_t *>(a.out) + ((size_t)b * n + h) * D + lane * PER;
