@@ -1,22 +1,25 @@
-"""bench.py — DistServe KV-cache data path on B200 (BASELINE.json configs[1]).
+"""bench.py — the DistServe KV-cache data path on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--impl ds|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2|1|3|4|5] [--batch B]
+                    [--impl ds|reference]
 
-One STEP = one pass of the whole hot path over one batch of B synthetic
-requests with OPT-13B attention geometry (40 layers x 40 heads x 128), prompt
-512 / output 64 (BASELINE config 2):
-  a1  block tables for the batch (prefill pool ALLOC; decode pool ALLOC/APPEND/FREE)
-  a2+a3  40 x ds_prefill_attn (one per layer, fused paged K/V write)
-  a4-a6  ds_kv_migrate of all 40 layers' pages prefill pool -> decode pool
-  a7+a8  64 decode steps x 40 layers of ds_decode_attn (append + split-K attention)
-At N=1 one GPU plays both instances (migration is the LOCAL page copy); at
-N>1 ranks [0, N/2) are prefill instances and [N/2, N) decode instances, paired
-r <-> r + N/2 (independent pairs, one p2p exchange per pair per step; the
-prefill of batch k+1 overlaps the decode of batch k).
+One STEP = one pass of the whole hot path over one batch
+of B synthetic requests:
+  a1     block tables (prefill pool ALLOC/FREE; decode pool ALLOC/APPEND/FREE)
+  a2+a3  ds_prefill_attn for every local layer (fused paged K/V write)
+  a4-a6  ds_kv_migrate of all local layers' pages, prefill pool -> decode pool
+  a7+a8  `output` decode steps x local layers of ds_decode_attn
+Default workload = BASELINE configs[1] (config 2): OPT-13B attention geometry
+(40 layers x 40 heads x 128), 16 requests x 512 prompt / 64 output.
+At N=1 one GPU plays both instances (migration = LOCAL page copy); at N>1
+ranks [0, N/2) are prefill and [N/2, N) decode instances, paired by
+paper_2401_09670_b200.pairing (same layers/heads), migration = NCCL
+p2p over NVLink; each replica pair serves its own batch (weak scaling) and the
+prefill of batch k+1 overlaps the decode of batch k.
 
-value = (prompt + generated) tokens of all pairs / max-over-ranks step time.
-Inputs are resident in HBM and larger than L2 (each layer's Q/K/V is 252 MB,
-each layer's decode KV ~180 MB, layers rotate), so no L2 flush is needed.
+value = (prompt + generated) tokens of all replicas / max-over-ranks step time.
+Inputs are resident and larger than L2 (per-layer prefill inputs and decode KV
+are >= ~180 MB and layers rotate), so no L2 flush is needed.
 """
 from __future__ import annotations
 
@@ -35,10 +38,26 @@ sys.path.insert(0, ROOT)
 
 import numpy as np  # noqa: E402
 
+import synthetic as syn  # noqa: E402
+
 METRIC = "prefill tok/s, decode tok/s/GPU, KV migrate GB/s at 1/2/4/8 B200 vs roofline"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
-NVLINK_GBS = 900.0  # nominal per direction per GPU (B200_PROFILING.md; measured peer copy 770)
+NVLINK_GBS = 900.0  # nominal per direction per GPU (770 measured peer copy, B200_PROFILING.md)
+
+# BASELINE.json configs. mix: prompt-length source; output = decode steps run.
+CONFIGS = {
+    "1": dict(geom=syn.TINY, mix="fixed", prompt=32, output=8, batch=1, tp=1, pp=1,
+              desc="config 1: 1 layer x 4 heads x 64, prompt 32 + 8 decode steps"),
+    "2": dict(geom=syn.OPT_13B, mix="fixed", prompt=512, output=64, batch=16, tp=1, pp=1,
+              desc="config 2: OPT-13B attention geometry, 512 in / 64 out"),
+    "3": dict(geom=syn.OPT_13B, mix="chatbot", prompt=0, output=64, batch=64, tp=1, pp=1,
+              desc="config 3: OPT-13B, ShareGPT-like chatbot length mix"),
+    "4": dict(geom=syn.OPT_66B, mix="code", prompt=0, output=64, batch=32, tp=2, pp=2,
+              desc="config 4: OPT-66B, HumanEval-like code lengths, TP2 x PP2 per phase"),
+    "5": dict(geom=syn.OPT_175B, mix="summarization", prompt=0, output=32, batch=8, tp=4, pp=1,
+              desc="config 5: OPT-175B, LongBench-like summarization lengths, TP4 -> TP4"),
+}
 
 
 def parse():
@@ -46,22 +65,22 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--batch", type=int, default=16)
-    p.add_argument("--prompt", type=int, default=512)
-    p.add_argument("--output", type=int, default=64)
+    p.add_argument("--config", default="2", choices=sorted(CONFIGS))
+    p.add_argument("--batch", type=int, default=0, help="requests per batch (0 = config default)")
+    p.add_argument("--prompt", type=int, default=0, help="fixed prompt length override")
+    p.add_argument("--output", type=int, default=0, help="decode steps override")
     p.add_argument("--impl", default="ds", choices=["ds", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--profile", action="store_true", help="one short pass for ncu (no JSON)")
     p.add_argument("--no-graphs", action="store_true", help="eager decode launches (no CUDA graphs)")
+    p.add_argument("--profile", action="store_true", help="one short pass for ncu (no JSON)")
     return p.parse_args()
 
 
 def load_peaks():
     try:
-        d = json.load(open(PEAKS_PATH))
-        return d, "measured"
+        return json.load(open(PEAKS_PATH)), "measured"
     except Exception:
         return FALLBACK_PEAKS, "fallback"
 
@@ -109,18 +128,38 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- workload
 class Workload:
-    """Synthetic OPT-13B-geometry batch; identical on every rank of a pair."""
+    """One batch of one replica on one rank: prompt lengths, decode steps and the
+    rank's local shard (layers of its PP stage, heads of its TP rank)."""
 
-    def __init__(self, batch, prompt, output, layers=40, heads=40, head_dim=128):
-        self.B, self.l0, self.out_len = batch, prompt, output
-        self.L, self.n, self.d = layers, heads, head_dim
-        self.lens = [prompt] * batch
-        self.T = prompt * batch
-        self.scale = 1.0 / math.sqrt(head_dim)
-        self.pages_per_seq = -(-prompt // 16)
-        self.maxb = -(-(prompt + output) // 16)
+    def __init__(self, cfg: dict, args, role):
+        g = cfg["geom"]
+        B = args.batch or cfg["batch"]
+        mix = "fixed" if args.prompt else cfg["mix"]
+        if mix == "fixed":
+            lens = [args.prompt or cfg["prompt"]] * B
+        elif mix == "chatbot":
+            lens = list(syn.lengths_chatbot(0, B)[0])
+        elif mix == "code":
+            inp = syn.lengths_code(0)[0]
+            lens = [int(inp[i % len(inp)]) for i in range(B)]
+        else:
+            lens = list(syn.lengths_summarization(0, B)[0])
+        self.cfg, self.mix, self.geom = cfg, mix, g
+        self.B, self.lens = B, [int(x) for x in lens]
+        self.out_len = args.output or cfg["output"]
+        self.L, self.n, self.d = role.layer_count, role.head_count, g.head_dim
+        self.L_full, self.n_full = g.layers, g.heads
+        self.T = sum(self.lens)
+        self.scale = 1.0 / math.sqrt(self.d)
+        self.pages = [-(-l // 16) for l in self.lens]
+        self.maxb = -(-(max(self.lens) + self.out_len) // 16)
+        self.max_len = max(self.lens)
 
-    # algorithmic work (SURVEY §8d; DESIGN.md "Roofline")
+    def describe(self):
+        return (f"{self.cfg['desc']}; {self.B} requests (prompt tokens {self.T}, max {self.max_len}), "
+                f"{self.out_len} decode steps; per GPU {self.L} layers x {self.n} heads x {self.d}")
+
+    # algorithmic work (SURVEY §8d, DESIGN.md §6)
     def prefill_flops_per_layer(self):
         return sum(self.n * 2 * self.d * l * (l + 1) for l in self.lens)
 
@@ -131,11 +170,11 @@ class Workload:
         pages = sum(-(-(c + 1) // 16) for c in ctx)
         return sum(self.n * (4 * c * self.d + 12 * self.d) for c in ctx) + 4 * pages
 
-    def kv_payload_bytes(self):  # valid tokens, all layers, K+V
+    def kv_payload_bytes(self):  # valid tokens, local layers and heads, K+V
         return 2 * self.L * self.T * self.n * self.d * 2
 
     def kv_page_bytes(self):  # whole pages actually moved
-        return 2 * self.L * self.B * self.pages_per_seq * 16 * self.n * self.d * 2
+        return 2 * self.L * sum(self.pages) * 16 * self.n * self.d * 2
 
 
 def _i32(torch, a):
@@ -143,28 +182,28 @@ def _i32(torch, a):
 
 
 class Engine:
-    """Device state of one rank: pools, resident inputs, staging, launch helpers."""
+    """Device state of one rank: pools, resident inputs, staging, CUDA graphs."""
 
-    def __init__(self, w: Workload, role: str, comm, peer, seed, torch, ds):
-        self.w, self.role, self.comm, self.peer, self.torch, self.ds = w, role, comm, peer, torch, ds
+    def __init__(self, w: Workload, role, comm, seed, torch, ds):
+        self.w, self.role, self.comm, self.torch, self.ds = w, role, comm, torch, ds
         dev = "cuda"
         bf = torch.bfloat16
         g = torch.Generator(device=dev)
         g.manual_seed(seed)
-        self.pf = role in ("both", "prefill")
-        self.dc = role in ("both", "decode")
+        self.pf = role.phase in ("both", "prefill")
+        self.dc = role.phase in ("both", "decode")
         # pools sized for 2 batches in flight (pipelined N>1) + headroom
         nb = 2 * w.B * w.maxb + 64
         if self.pf:
             self.P = ds.KVCache.empty(w.L, nb, w.n, w.d)
             self.pool_p = ds.Pool(nb)
             shape = (w.T, w.n, w.d)
-            # per-layer resident prefill inputs (N(0,1) bf16; each layer 3 x 84 MB)
+            # per-layer resident prefill inputs, N(0,1) bf16
             self.q = [torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(bf) for _ in range(w.L)]
             self.k = [torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(bf) for _ in range(w.L)]
             self.v = [torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(bf) for _ in range(w.L)]
             self.out = torch.empty(shape, dtype=bf, device=dev)
-            self.cu = _i32(torch, np.concatenate([[0], np.cumsum(w.lens)]))
+            self.cu = _i32(torch, syn.cu_seqlens(w.lens))
         if self.dc:
             self.D = ds.KVCache.empty(w.L, nb, w.n, w.d)
             self.pool_d = ds.Pool(nb)
@@ -173,7 +212,7 @@ class Engine:
             self.dk = torch.randn(dshape, generator=g, device=dev, dtype=torch.float32).to(bf)
             self.dv = torch.randn(dshape, generator=g, device=dev, dtype=torch.float32).to(bf)
             self.dout = torch.empty((w.out_len, w.B, w.n, w.d), dtype=bf, device=dev)
-            self.max_c = w.l0 + w.out_len - 1  # largest cache length of the batch (validation only)
+            self.max_c = w.max_len + w.out_len - 1  # largest cache length of the batch (validation only)
             self.ws = torch.zeros(max(16, ds.ds_decode_workspace_bytes(w.B, w.n, w.d, self.max_c)),
                                   dtype=torch.uint8, device=dev)
             # fixed device block table / lengths read by the captured decode graphs
@@ -184,25 +223,36 @@ class Engine:
             self.h_ev2 = [None, None]
             self.hslot = 0
             self.graphs = None
-        nblk = w.B * w.pages_per_seq
-        mrole = {"both": ds.DS_MIGRATE_LOCAL, "prefill": ds.DS_MIGRATE_SEND, "decode": ds.DS_MIGRATE_RECV}[role]
-        self.mrole = mrole
+        nblk = sum(w.pages)
+        self.mrole = {"both": ds.DS_MIGRATE_LOCAL, "prefill": ds.DS_MIGRATE_SEND,
+                      "decode": ds.DS_MIGRATE_RECV}[role.phase]
         cache_for_size = self.P if self.pf else self.D
-        sbytes = ds.ds_kv_migrate_staging_bytes(cache_for_size, mrole, w.L, nblk, w.n)
+        sbytes = ds.ds_kv_migrate_staging_bytes(cache_for_size, self.mrole, w.L, nblk, w.n)
         self.staging = torch.empty(sbytes, dtype=torch.uint8, device=dev) if sbytes else None
-        # pinned host ring for the per-step block-table / cache-length uploads (async H2D)
-        self.ring = w.out_len + 2
+        # pinned host ring for prefill / admission table uploads (async H2D)
+        self.ring = 4
         self.h_tab = torch.empty((self.ring, w.B, w.maxb), dtype=torch.int32).pin_memory()
-        self.h_len = torch.empty((self.ring, w.B), dtype=torch.int32).pin_memory()
         self.d_tab = torch.empty((self.ring, w.B, w.maxb), dtype=torch.int32, device=dev)
-        self.d_len = torch.empty((self.ring, w.B), dtype=torch.int32, device=dev)
         self.h_ev = [None] * self.ring
         self.slot = 0
-        self.stream = torch.cuda.current_stream()
         self.launches = 0
-        self.decode_events = []
+        idx = np.concatenate([np.arange(b * w.maxb, b * w.maxb + p) for b, p in enumerate(w.pages)])
+        self._idx = _i32(torch, idx).long()
 
-    def upload_fixed(self, table: np.ndarray, lens):
+    # -- host -> device block tables ------------------------------------------------
+    def upload(self, table: np.ndarray):
+        s = self.slot
+        self.slot = (s + 1) % self.ring
+        if self.h_ev[s] is not None:
+            self.h_ev[s].synchronize()  # the previous copy out of this slot has completed
+        self.h_tab[s].numpy()[:] = table
+        self.d_tab[s].copy_(self.h_tab[s], non_blocking=True)
+        ev = self.torch.cuda.Event()
+        ev.record()
+        self.h_ev[s] = ev
+        return self.d_tab[s]
+
+    def upload_decode(self, table: np.ndarray, lens):
         """async H2D of the decode block table + lengths into the graphs' fixed buffers"""
         i = self.hslot
         self.hslot ^= 1
@@ -216,15 +266,20 @@ class Engine:
         ev.record()
         self.h_ev2[i] = ev
 
+    def page_ids(self, table_dev):
+        """the batch's page ids in logical order (device gather of the table rows)"""
+        return table_dev.reshape(-1).index_select(0, self._idx).contiguous()
+
+    # -- decode ---------------------------------------------------------------------
     def decode_layers(self, s):
-        """ds_decode_attn for every layer of decode step s (reads dtab / dlen)"""
+        """ds_decode_attn for every local layer of decode step s (reads dtab / dlen)"""
         w, ds = self.w, self.ds
         for layer in range(w.L):
             ds.ds_decode_attn(self.dq[s, layer], self.dk[s, layer], self.dv[s, layer], self.dout[s], self.D, layer,
                               self.dtab, self.dlen, self.max_c, w.scale, self.ws)
 
     def capture_decode_graphs(self):
-        """one CUDA graph per decode step: the 40-layer loop becomes a single launch"""
+        """one CUDA graph per decode step: the layer loop becomes a single launch"""
         torch = self.torch
         self.graphs = []
         for s in range(self.w.out_len):
@@ -234,76 +289,60 @@ class Engine:
             self.graphs.append(g)
         torch.cuda.synchronize()
 
-    def upload(self, table: np.ndarray, lens):
-        """async H2D of a block table (+ lengths) through the pinned ring"""
-        s = self.slot
-        self.slot = (s + 1) % self.ring
-        if self.h_ev[s] is not None:
-            self.h_ev[s].synchronize()  # the previous copy out of this slot has completed
-        self.h_tab[s].numpy()[:, :table.shape[1]] = table
-        self.h_len[s].numpy()[:] = lens
-        self.d_tab[s].copy_(self.h_tab[s], non_blocking=True)
-        self.d_len[s].copy_(self.h_len[s], non_blocking=True)
-        ev = self.torch.cuda.Event()
-        ev.record()
-        self.h_ev[s] = ev
-        return self.d_tab[s], self.d_len[s]
-
-    # -- one step ------------------------------------------------------------------
-    def step(self, events=None, time_decode=False):
-        torch, ds, w = self.torch, self.ds, self.w
+    # -- one step -------------------------------------------------------------------
+    def step(self, events=None):
+        ds, w, role = self.ds, self.w, self.role
         ev = events or {}
-        nblk = w.B * w.pages_per_seq
         if "start" in ev:
             ev["start"].record()
-        if self.pf:
+        if self.pf:  # a1 + a2/a3
             tp = np.full((w.B, w.maxb), -1, np.int32)
             ds.ds_block_table(self.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
-            tp_d, _ = self.upload(tp, w.lens)
+            tp_d = self.upload(tp)
             for layer in range(w.L):
-                ds.ds_prefill_attn(self.q[layer], self.k[layer], self.v[layer], self.out, self.cu, w.l0, self.P, layer,
-                                   tp_d, w.scale)
+                ds.ds_prefill_attn(self.q[layer], self.k[layer], self.v[layer], self.out, self.cu, w.max_len,
+                                   self.P, layer, tp_d, w.scale)
             self.launches += w.L
-            src_ids = tp_d[:, :w.pages_per_seq].reshape(-1).contiguous()
+            src_ids = self.page_ids(tp_d)
         if "prefill_end" in ev:
             ev["prefill_end"].record()
-        if self.dc:
+        if self.dc:  # admission on the decode side (pull)
             td = np.full((w.B, w.maxb), -1, np.int32)
             ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, [0] * w.B, w.lens, td)
-            td_d, _ = self.upload(td, w.lens)
-            dst_ids = td_d[:, :w.pages_per_seq].reshape(-1).contiguous()
-        # migration (pull, P:382: the decode side has admitted the batch above)
+            dst_ids = self.page_ids(self.upload(td))
+        # a4-a6
         if self.mrole == ds.DS_MIGRATE_LOCAL:
             ds.ds_kv_migrate(None, self.mrole, 0, self.P, 0, w.L, src_ids, 0, w.n, None,
                              dst_cache=self.D, dst_block_ids=dst_ids)
             self.launches += 1
         else:
             chunk_rows = max(1, (64 << 20) // (w.n * 16 * w.d * 2))
-            self.launches += -(-(2 * w.L * nblk) // chunk_rows)  # pack or unpack kernels (+ NCCL's own)
+            self.launches += -(-(2 * w.L * sum(w.pages)) // chunk_rows)  # pack or unpack kernels (+ NCCL's)
             if self.pf:
-                ds.ds_kv_migrate(self.comm, self.mrole, self.peer, self.P, 0, w.L, src_ids, 0, w.n, self.staging)
+                ds.ds_kv_migrate(self.comm, self.mrole, role.peer, self.P, 0, w.L, src_ids, 0, w.n, self.staging)
             else:
-                ds.ds_kv_migrate(self.comm, self.mrole, self.peer, self.D, 0, w.L, dst_ids, 0, w.n, self.staging)
+                ds.ds_kv_migrate(self.comm, self.mrole, role.peer, self.D, 0, w.L, dst_ids, 0, w.n, self.staging)
         if self.pf:
             ds.ds_block_table(self.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
         if "migrate_end" in ev:
             ev["migrate_end"].record()
-        if self.dc:
+        if self.dc:  # a1 (APPEND per step) + a7/a8
             cur = list(w.lens)
             for s in range(w.out_len):
                 ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, cur, [1] * w.B, td)
-                self.upload_fixed(td, cur)
+                self.upload_decode(td, cur)
                 if self.graphs is not None:
                     self.graphs[s].replay()
                 else:
                     self.decode_layers(s)
-                self.launches += 2 * w.L  # decode_kernel + decode_combine_kernel per layer
+                self.launches += w.L  # one decode_kernel per layer (split merge fused)
                 cur = [c + 1 for c in cur]
             ds.ds_block_table(self.pool_d, ds.DS_BT_FREE, cur, None, td)
         if "end" in ev:
             ev["end"].record()
 
 
+# ----------------------------------------------------------------------------- distributed
 def dist_setup(args):
     import torch
     import torch.distributed as dist
@@ -312,29 +351,10 @@ def dist_setup(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    if world > 1 and world % 2:
-        raise SystemExit("N>1 needs an even number of GPUs (prefill/decode pairs)")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
-
-
-def pair_of(rank, world):
-    """(role, peer): ranks [0, N/2) prefill, [N/2, N) decode; pair r <-> r + N/2."""
-    if world == 1:
-        return "both", 0
-    half = world // 2
-    return ("prefill", rank + half) if rank < half else ("decode", rank - half)
-
-
-def make_comm(world, rank, ds):
-    import torch.distributed as dist
-    if world == 1:
-        return None  # both instances on one GPU: LOCAL page copy, no communicator
-    obj = [ds.ds_comm_get_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
-    return ds.ds_comm_init(obj[0], world, rank)
 
 
 def max_over_ranks(x, world):
@@ -356,21 +376,23 @@ def barrier(world):
 # ----------------------------------------------------------------------------- CPU oracle
 def oracle_sample_tok_s(w: Workload, target_s: float = 15.0):
     """Time the fp64 C oracle (as it stands) on a bounded sample of the same
-    workload and scale linearly to tok/s: prefill of one 512-token request over
-    all 40 heads of one layer, plus decode steps (c = 512..) of one request over
-    one layer. Work is linear in layers, heads and requests."""
+    workload and scale linearly to tok/s: prefill of the batch's longest request
+    over all local heads of one layer, plus decode steps of it over one layer.
+    Work is linear in layers and heads; requests are scaled by their cost share
+    (l(l+1) for prefill, context length for decode)."""
     import oracle
-    import synthetic as syn
     threads = os.cpu_count() or 1
-    b = syn.prefill_batch(0, [w.l0], w.n, w.d)
+    l0 = w.max_len
+    b = syn.prefill_batch(0, [l0], w.n, w.d)
     t0 = time.perf_counter()
     oracle.prefill(b.q, b.k, b.v, b.cu_seqlens, w.scale, nthreads=threads)
-    t_pf = time.perf_counter() - t0  # one request, one layer
-    pool = oracle.Pool(1, w.pages_per_seq + w.out_len // 16 + 2, w.n, w.d)
-    table = np.full((1, w.maxb + 1), -1, np.int32)
-    pool.append([0], [w.l0], table)
+    t_pf = time.perf_counter() - t0
+    cols = -(-(l0 + w.out_len + 1) // 16)
+    pool = oracle.Pool(1, cols + 1, w.n, w.d)
+    table = np.full((1, cols), -1, np.int32)
+    pool.append([0], [l0], table)
     pool.write_prefill(0, b.k, b.v, b.cu_seqlens, table)
-    n_dec, t_dec, c = 0, 0.0, w.l0
+    n_dec, t_dec, c = 0, 0.0, l0
     while n_dec < w.out_len and t_dec < target_s:
         pool.append([c], [1], table)
         db = syn.decode_batch(n_dec, 1, w.n, w.d)
@@ -379,31 +401,52 @@ def oracle_sample_tok_s(w: Workload, target_s: float = 15.0):
         t_dec += time.perf_counter() - t0
         c += 1
         n_dec += 1
-    per_req = w.L * (t_pf + t_dec / n_dec * w.out_len)  # all layers, one request
-    tok_s = (w.l0 + w.out_len) / per_req
-    sample = (f"1 request x 1 layer x {w.n} heads: prefill {w.l0} tokens ({t_pf:.2f} s) + {n_dec} decode steps "
-              f"({t_dec:.2f} s); scaled linearly to {w.L} layers and {w.out_len} steps")
-    return tok_s, threads, sample, t_pf + t_dec
+    pf_all = t_pf * sum(l * (l + 1) for l in w.lens) / (l0 * (l0 + 1))
+    dec_all = (t_dec / n_dec) * w.out_len * sum(w.lens) / l0
+    per_batch = w.L_full * (w.n_full / w.n) * (pf_all + dec_all)  # all layers and heads of the model
+    tok_s = (w.T + w.B * w.out_len) / per_batch
+    sample = (f"1 request ({l0} tokens) x 1 layer x {w.n} heads: prefill ({t_pf:.2f} s) + {n_dec} decode steps "
+              f"({t_dec:.2f} s) with {threads} threads; scaled linearly to the batch and all "
+              f"{w.L_full} layers x {w.n_full} heads")
+    return tok_s, threads, sample
 
 
-# ----------------------------------------------------------------------------- main arms
+# ----------------------------------------------------------------------------- arms
+def _config_line(w, world, replicas):
+    tp, pp = (1, 1) if world == 1 else (w.cfg["tp"], w.cfg["pp"])
+    return {"workload": w.describe(), "batch": w.B, "prompt_tokens": w.T, "max_prompt": w.max_len,
+            "decode_steps": w.out_len, "mix": w.mix, "replicas": replicas, "tp": tp, "pp": pp,
+            "parallelism": "single GPU (P+D)" if world == 1 else
+            f"{replicas} replica pair(s) x TP{tp} PP{pp} prefill -> TP{tp} PP{pp} decode",
+            "l2": "inputs larger than L2; no flush"}
+
+
+def _role_for(cfg, rank, world):
+    from paper_2401_09670_b200.pairing import assign
+    g = cfg["geom"]
+    if world == 1:
+        return assign(0, 1, g.layers, g.heads)
+    return assign(rank, world, g.layers, g.heads, cfg["tp"], cfg["pp"])
+
+
 def run_reference(args):
-    """--impl reference: the oracle as it stands on the host cores, same config/metric."""
+    """--impl reference: the oracle as it stands on the host cores, same config and metric."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    w = Workload(args.batch, args.prompt, args.output)
-    vals = []
+    cfg = CONFIGS[args.config]
+    w = Workload(cfg, args, _role_for(cfg, 0, world))
+    vals, sample, threads = [], "", 1
     for _ in range(max(args.steps, 1)):
-        tok_s, threads, sample, spent = oracle_sample_tok_s(w, target_s=5.0)
-        vals.append(tok_s * w.B / w.B)  # per-request rate == whole-batch rate (linear)
+        tok_s, threads, sample = oracle_sample_tok_s(w, target_s=4.0)
+        vals.append(tok_s)
     v = statistics.median(vals)
+    replicas = 1 if world == 1 else world // 2 // (cfg["tp"] * cfg["pp"])
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tok/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": w.B * (w.l0 + w.out_len) / v * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"OPT-13B attention geometry, {w.B} req x {w.l0} in / {w.out_len} out",
-                       "batch": w.B, "prompt": w.l0, "output": w.out_len},
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": (w.T + w.B * w.out_len) / v * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config_line(w, world, replicas),
             "cpu_baseline": {"value": v, "unit": "tok/s", "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -413,10 +456,18 @@ def run_ds(args):
     import torch
     world, rank, local = dist_setup(args)
     import paper_2401_09670_b200 as ds
-    role, peer = pair_of(rank, world)
-    w = Workload(args.batch, args.prompt, args.output)
-    comm = make_comm(world, rank, ds)
-    eng = Engine(w, role, comm, peer, seed=1234 + (rank % max(1, world // 2)), torch=torch, ds=ds)
+    from paper_2401_09670_b200 import pairing
+    cfg = CONFIGS[args.config]
+    role = _role_for(cfg, rank, world)
+    w = Workload(cfg, args, role)
+    if world == 1:
+        comm = None  # both instances on one GPU: LOCAL page copy, no communicator
+    else:
+        import torch.distributed as dist
+        comm = ds.ds_comm_init(pairing.bootstrap_unique_id(ds.ds_comm_get_unique_id, rank, world, dist), world, rank)
+    replicas = 1 if world == 1 else world // 2 // (cfg["tp"] * cfg["pp"])
+    eng = Engine(w, role, comm, seed=1234 + role.replica * 7919 + role.stage * 131 + role.tp_rank, torch=torch,
+                 ds=ds)
     torch.cuda.synchronize()
     if args.profile:
         eng.step()
@@ -434,13 +485,12 @@ def run_ds(args):
     sampler.start()
     phase = []
     eng.launches = 0
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
     t_start.record()
-    for s in range(args.steps):
+    for _ in range(args.steps):
         evs = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "prefill_end", "migrate_end", "end")}
         eng.step(evs)
         phase.append(evs)
@@ -448,67 +498,84 @@ def run_ds(args):
     torch.cuda.synchronize()
     barrier(world)
     clocks = sampler.stop()
-    total_ms = t_start.elapsed_time(t_end)
-    total_ms = max_over_ranks(total_ms, world)
-    launches = eng.launches
+    total_ms = max_over_ranks(t_start.elapsed_time(t_end), world)
     ms_step = total_ms / args.steps
-    pairs = max(1, world // 2)
-    tokens_step = pairs * w.B * (w.l0 + w.out_len)
-    value = tokens_step / (ms_step / 1e3)
+    value = replicas * (w.T + w.B * w.out_len) / (ms_step / 1e3)
 
     peaks, peak_kind = load_peaks()
-    comp = {}
-    # phase breakdown on this rank (device time between events)
+    comp = {"phase": role.phase}
+    med = lambda a, b: statistics.median(e[a].elapsed_time(e[b]) for e in phase)  # noqa: E731
     if eng.pf:
-        pf_ms = statistics.median(e["start"].elapsed_time(e["prefill_end"]) for e in phase)
+        pf_ms = med("start", "prefill_end")
         comp["prefill_ms_per_step"] = pf_ms
         comp["prefill_tok_s_per_gpu"] = w.T / (pf_ms / 1e3)
         comp["prefill_tflops"] = w.L * w.prefill_flops_per_layer() / (pf_ms / 1e3) / 1e12
         comp["prefill_frac_of_tensor_peak"] = comp["prefill_tflops"] / peaks["bf16_tflops"]
-        t_roof = max(w.prefill_flops_per_layer() / (peaks["bf16_tflops"] * 1e12),
-                     w.prefill_bytes_per_layer() / (peaks["hbm_gbs"] * 1e9)) * w.L
+        t_roof = w.L * max(w.prefill_flops_per_layer() / (peaks["bf16_tflops"] * 1e12),
+                           w.prefill_bytes_per_layer() / (peaks["hbm_gbs"] * 1e9))
         comp["prefill_frac_of_attainable_roofline"] = t_roof / (pf_ms / 1e3)
-        mig_ms = statistics.median(e["prefill_end"].elapsed_time(e["migrate_end"]) for e in phase)
+        mig_ms = med("prefill_end", "migrate_end")
         comp["migrate_ms_per_step"] = mig_ms
         comp["kv_migrate_GBps"] = w.kv_payload_bytes() / (mig_ms / 1e3) / 1e9
         comp["kv_migrate_page_GBps"] = w.kv_page_bytes() / (mig_ms / 1e3) / 1e9
+        comp["kv_migrate_path"] = "LOCAL page copy (one GPU)" if world == 1 else "NCCL p2p over NVLink"
+        if world > 1:
+            comp["kv_migrate_frac_of_nvlink"] = comp["kv_migrate_page_GBps"] / NVLINK_GBS
     dec_kernel = None
     if eng.dc:
-        dec_ms = statistics.median(e["migrate_end"].elapsed_time(e["end"]) for e in phase)
+        dec_ms = med("migrate_end", "end")
         comp["decode_ms_per_step"] = dec_ms
         comp["decode_tok_s_per_gpu"] = w.B * w.out_len / (dec_ms / 1e3)
         ctx_steps = [[c + s for c in w.lens] for s in range(w.out_len)]
         avg_bytes = sum(w.decode_bytes(c) for c in ctx_steps) / w.out_len
-        avg_ms = dec_ms / (w.out_len * w.L)  # device time per ds_decode_attn call (both kernels + gaps)
+        avg_ms = dec_ms / (w.out_len * w.L)  # device time per ds_decode_attn call (incl. table upload, gaps)
         dec_kernel = (avg_bytes, avg_ms)
         comp["decode_attn_GBps"] = avg_bytes / (avg_ms / 1e3) / 1e9
         comp["decode_attn_frac_of_hbm"] = comp["decode_attn_GBps"] / peaks["hbm_gbs"]
         comp["decode_attn_us_per_launch"] = avg_ms * 1e3
         comp["decode_graphs"] = eng.graphs is not None
-    roofline = None
+    roofline = None  # the dominant kernel of this rank's step
     if dec_kernel:
         achieved = dec_kernel[0] / (dec_kernel[1] / 1e3) / 1e9
-        roofline = {"kernel": "ds_decode_attn (decode_kernel + decode_combine_kernel)", "bound": "hbm", "achieved": achieved,
-                    "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                    "traffic": None, "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
+        roofline = {"kernel": "ds_decode_attn (decode_kernel, split merge fused)", "bound": "hbm",
+                    "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                    "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                     "algorithmic_bytes_per_launch": dec_kernel[0]}
+    elif eng.pf:
+        t_layer = comp["prefill_ms_per_step"] / w.L / 1e3
+        fl, by = w.prefill_flops_per_layer(), w.prefill_bytes_per_layer()
+        if fl / by >= peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9):
+            roofline = {"kernel": "ds_prefill_attn (prefill_kernel)", "bound": "tensor",
+                        "achieved": fl / t_layer / 1e12, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                        "frac": fl / t_layer / 1e12 / peaks["bf16_tflops"], "traffic": None}
+        else:
+            roofline = {"kernel": "ds_prefill_attn (prefill_kernel)", "bound": "hbm", "achieved": by / t_layer / 1e9,
+                        "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": by / t_layer / 1e9 / peaks["hbm_gbs"],
+                        "traffic": None}
     line = {"metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"OPT-13B attention geometry (40 layers x 40 heads x 128), "
-                                   f"{w.B} requests x {w.l0} prompt / {w.out_len} output per pair; "
-                                   f"prefill->migrate->decode per step",
-                       "batch": w.B, "prompt": w.l0, "output": w.out_len, "pairs": pairs,
-                       "parallelism": "single GPU (P+D)" if world == 1 else f"{pairs}P:{pairs}D pairs",
-                       "l2": "inputs larger than L2 (252 MB/layer prefill, ~180 MB/layer decode KV)"},
-            "components": comp, "roofline": roofline, "clocks": clocks, "gpu_launches": launches}
-    # e2e through the public API with host buffers
+            "config": _config_line(w, world, replicas), "components": comp, "roofline": roofline,
+            "clocks": clocks, "gpu_launches": eng.launches}
     if not args.no_e2e:
-        line["e2e"] = run_e2e(args, eng, w, world, torch, ds)
+        line["e2e"] = run_e2e(args, eng, w, world, replicas, torch)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        tok_s, threads, sample, _ = oracle_sample_tok_s(w)
+        tok_s, threads, sample = oracle_sample_tok_s(w)
         line["cpu_baseline"] = {"value": tok_s, "unit": "tok/s", "cores": threads, "kind": "oracle",
                                 "sample": sample}
+    if world > 1:  # every rank's components (prefill ranks report migrate, decode ranks decode)
+        import torch.distributed as dist
+        objs = [None] * world
+        dist.all_gather_object(objs, comp)
+        line["components_by_rank"] = {str(r): c for r, c in enumerate(objs)}
+        decs = [c for c in objs if "decode_attn_GBps" in c]
+        if decs:  # the decode kernel dominates the job; report it from the first decode rank
+            d0 = decs[0]
+            line["roofline"] = {"kernel": "ds_decode_attn (decode_kernel, split merge fused)", "bound": "hbm",
+                                "achieved": d0["decode_attn_GBps"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                "frac": d0["decode_attn_GBps"] / peaks["hbm_gbs"], "traffic": None,
+                                "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if comm is not None:
@@ -518,18 +585,18 @@ def run_ds(args):
         dist.destroy_process_group()
 
 
-def run_e2e(args, eng, w, world, torch, ds):
-    """Same step, but every layer's prefill inputs are copied host(pinned)->device
-    and the decode inputs too; the last layer's decode outputs are read back."""
+def run_e2e(args, eng, w, world, replicas, torch):
+    """The same step through the same API, but every layer's prefill inputs and
+    every decode step's inputs are copied host(pinned)->device inside the timed
+    region, and the decode outputs are read back."""
     bf = torch.bfloat16
     h2d = d2h = 0
     host = {}
     if eng.pf:
-        shape = (w.T, w.n, w.d)
-        host["qkv"] = torch.randn((3,) + shape, dtype=torch.float32).to(bf).pin_memory()
+        host["qkv"] = torch.randn((3, w.T, w.n, w.d), dtype=torch.float32).to(bf).pin_memory()
     if eng.dc:
-        host["dec"] = torch.randn((3, w.out_len, w.L, w.B, w.n, w.d), dtype=torch.float32).to(bf).pin_memory()
-        host["out"] = torch.empty((w.out_len, w.B, w.n, w.d), dtype=bf).pin_memory()
+        host["dec"] = torch.randn((3,) + tuple(eng.dq.shape), dtype=torch.float32).to(bf).pin_memory()
+        host["out"] = torch.empty(tuple(eng.dout.shape), dtype=bf).pin_memory()
 
     def step():
         nonlocal h2d, d2h
@@ -560,8 +627,7 @@ def run_e2e(args, eng, w, world, torch, ds):
     e1.record()
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), world) / args.e2e_steps
-    pairs = max(1, world // 2)
-    return {"value": pairs * w.B * (w.l0 + w.out_len) / (ms / 1e3), "unit": "tok/s",
+    return {"value": replicas * (w.T + w.B * w.out_len) / (ms / 1e3), "unit": "tok/s",
             "h2d_bytes_per_step": h2d // args.e2e_steps, "d2h_bytes_per_step": d2h // args.e2e_steps,
             "ms_per_step": ms, "steps": args.e2e_steps}
 

@@ -1,0 +1,90 @@
+"""Multi-process host logic on CPU (gloo, world_size 2 and 4): rank roles and
+prefill<->decode pairing, the NCCL unique-id bootstrap
+through torch.distributed, and the max-over-ranks timing reduction used by
+bench.py. The NCCL data path itself needs GPUs (tests/test_gpu_parity.py covers
+SELF/LOCAL on one GPU)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2401_09670_b200 import pairing
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        role = pairing.assign(rank, world, layers=40, heads=40)
+        # unique id: rank 0's bytes reach everybody unchanged
+        uid = pairing.bootstrap_unique_id(lambda: bytes(range(128)) if rank == 0 else None, rank, world, dist)
+        # max over ranks (bench.py reduces the device time this way)
+        t = torch.tensor([float(rank + 1) * 1.5], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        # each pair exchanges its (layer, head) ranges: they must agree (corresponding layers)
+        mine = torch.tensor([role.layer_begin, role.layer_count, role.head_begin, role.head_count])
+        theirs = torch.zeros_like(mine)
+        if role.phase == "prefill":
+            dist.send(mine, role.peer)
+            dist.recv(theirs, role.peer)
+        else:
+            dist.recv(theirs, role.peer)
+            dist.send(mine, role.peer)
+        q.put((rank, role.phase, role.peer, uid, float(t.item()), bool(torch.equal(mine, theirs))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_pairing_bootstrap_and_max(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    half = world // 2
+    for rank, phase, peer, uid, tmax, same in res:
+        assert phase == ("prefill" if rank < half else "decode")
+        assert peer == (rank + half if rank < half else rank - half)
+        assert uid == bytes(range(128))
+        assert tmax == world * 1.5
+        assert same
+
+
+@pytest.mark.parametrize("world,layers,heads,tp,pp", [
+    (1, 40, 40, 1, 1), (2, 40, 40, 1, 1), (8, 40, 40, 1, 1),   # config 3: 1:1 .. 4:4 replicas
+    (8, 64, 72, 2, 2),                                          # config 4: OPT-66B TP2 x PP2 per phase
+    (8, 96, 96, 4, 1),                                          # config 5: OPT-175B TP4 -> TP4
+])
+def test_placements_pair_corresponding_layers_and_heads(world, layers, heads, tp, pp):
+    roles = pairing.all_roles(world, layers, heads, tp, pp)
+    pairing.check_pairing(roles)
+    if world > 1:
+        per_phase = sum(r.layer_count * r.head_count for r in roles if r.phase == "prefill")
+        assert per_phase == (world // 2) // (tp * pp) * layers * heads
+    if (tp, pp) == (2, 2):
+        r = pairing.assign(5, 8, layers, heads, tp, pp)  # decode rank 5 = replica 0, stage 0, tp 1
+        assert (r.stage, r.tp_rank, r.layer_begin, r.layer_count, r.head_begin, r.head_count) == (0, 1, 0, 32, 36, 36)
+        assert r.peer == 1
+
+
+def test_bad_placements_rejected():
+    for args in ((3, 40, 40, 1, 1), (4, 40, 40, 3, 1), (8, 40, 40, 1, 3), (6, 40, 40, 2, 1)):
+        with pytest.raises(ValueError):
+            pairing.all_roles(*args)
