@@ -193,7 +193,7 @@ class Engine:
         self.pf = role.phase in ("both", "prefill")
         self.dc = role.phase in ("both", "decode")
         # pools sized for 2 batches in flight (pipelined N>1) + headroom
-        nb = 2 * w.B * w.maxb + 64
+        nb = 2 * sum(-(-(l + w.out_len) // 16) for l in w.lens) + 64
         if self.pf:
             self.P = ds.KVCache.empty(w.L, nb, w.n, w.d)
             self.pool_p = ds.Pool(nb)
