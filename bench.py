@@ -18,8 +18,9 @@ p2p over NVLink; each replica pair serves its own batch (weak scaling) and the
 prefill of batch k+1 overlaps the decode of batch k.
 
 value = (prompt + generated) tokens of all replicas / max-over-ranks step time.
-Inputs are resident and larger than L2 (per-layer prefill inputs and decode KV
-are >= ~180 MB and layers rotate), so no L2 flush is needed.
+Inputs are resident and larger than L2: prefill inputs rotate over >= 1 GB of
+distinct buffers, each layer's decode KV is >= ~180 MB at B = 16 and the 40
+layers rotate, so no L2 flush is needed.
 """
 from __future__ import annotations
 
@@ -192,21 +193,26 @@ class Engine:
         g.manual_seed(seed)
         self.pf = role.phase in ("both", "prefill")
         self.dc = role.phase in ("both", "decode")
-        # pools sized for 2 batches in flight (pipelined N>1) + headroom
-        nb = 2 * sum(-(-(l + w.out_len) // 16) for l in w.lens) + 64
+        # one batch per pool: the prefill side's pages are reused for batch k+1 only after
+        # the (stream-ordered) migration of batch k; the decode side admits k+1 after k ends
+        nb_p = sum(w.pages) + 16
+        nb_d = sum(-(-(l + w.out_len) // 16) for l in w.lens) + 16
         if self.pf:
-            self.P = ds.KVCache.empty(w.L, nb, w.n, w.d)
-            self.pool_p = ds.Pool(nb)
+            self.P = ds.KVCache.empty(w.L, nb_p, w.n, w.d)
+            self.pool_p = ds.Pool(nb_p)
             shape = (w.T, w.n, w.d)
-            # per-layer resident prefill inputs, N(0,1) bf16
-            self.q = [torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(bf) for _ in range(w.L)]
-            self.k = [torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(bf) for _ in range(w.L)]
-            self.v = [torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(bf) for _ in range(w.L)]
+            # resident prefill inputs, N(0,1) bf16: distinct buffers rotate over the layers,
+            # enough of them (>= 2, >= 1 GB) that no layer's inputs are still in the 126 MB L2
+            per_layer = 3 * w.T * w.n * w.d * 2
+            n_in = min(w.L, max(2, -(-(1 << 30) // per_layer)))
+            self.q = [torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(bf) for _ in range(n_in)]
+            self.k = [torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(bf) for _ in range(n_in)]
+            self.v = [torch.randn(shape, generator=g, device=dev, dtype=torch.float32).to(bf) for _ in range(n_in)]
             self.out = torch.empty(shape, dtype=bf, device=dev)
             self.cu = _i32(torch, syn.cu_seqlens(w.lens))
         if self.dc:
-            self.D = ds.KVCache.empty(w.L, nb, w.n, w.d)
-            self.pool_d = ds.Pool(nb)
+            self.D = ds.KVCache.empty(w.L, nb_d, w.n, w.d)
+            self.pool_d = ds.Pool(nb_d)
             dshape = (w.out_len, w.L, w.B, w.n, w.d)
             self.dq = torch.randn(dshape, generator=g, device=dev, dtype=torch.float32).to(bf)
             self.dk = torch.randn(dshape, generator=g, device=dev, dtype=torch.float32).to(bf)
@@ -300,7 +306,8 @@ class Engine:
             ds.ds_block_table(self.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
             tp_d = self.upload(tp)
             for layer in range(w.L):
-                ds.ds_prefill_attn(self.q[layer], self.k[layer], self.v[layer], self.out, self.cu, w.max_len,
+                i = layer % len(self.q)
+                ds.ds_prefill_attn(self.q[i], self.k[i], self.v[i], self.out, self.cu, w.max_len,
                                    self.P, layer, tp_d, w.scale)
             self.launches += w.L
             src_ids = self.page_ids(tp_d)
@@ -600,11 +607,12 @@ def run_e2e(args, eng, w, world, replicas, torch):
 
     def step():
         nonlocal h2d, d2h
-        if eng.pf:
+        if eng.pf:  # every layer's inputs cross PCIe (into the rotating resident buffers)
             for layer in range(w.L):
-                eng.q[layer].copy_(host["qkv"][0], non_blocking=True)
-                eng.k[layer].copy_(host["qkv"][1], non_blocking=True)
-                eng.v[layer].copy_(host["qkv"][2], non_blocking=True)
+                i = layer % len(eng.q)
+                eng.q[i].copy_(host["qkv"][0], non_blocking=True)
+                eng.k[i].copy_(host["qkv"][1], non_blocking=True)
+                eng.v[i].copy_(host["qkv"][2], non_blocking=True)
                 h2d += 3 * host["qkv"][0].numel() * 2
         if eng.dc:
             eng.dq.copy_(host["dec"][0], non_blocking=True)
