@@ -6,20 +6,21 @@
 //   out[i] = sum_{j<=i} softmax_j(scale * q[i].k[j]) v[j]     per (sequence, head)
 //   cache[layer][K|V][bt[r][t/16]][h][t%16] = k|v[t][h]       (a3)
 //
-// B200 design (one CTA per (head, sequence, 128-row q tile), heaviest tiles first):
-//   warp 4  : TMA producer — Q tile once, then K_j / V_j tiles (j = 0..i, causal)
-//             into a 2-stage ring; after the loop it writes the diagonal K/V tile
-//             (the only one this CTA owns) into the paged cache with TMA tensor
-//             stores, one 16-token page per store (a3 fused: no extra HBM read).
-//   warp 5  : MMA issuer (one elected lane) — S_j = Q K_j^T into a double-buffered
-//             TMEM S (128x128 fp32), then O += P_{j-1} V_{j-1} into TMEM O; commits
-//             to mbarriers.
-//   warps 0-3: softmax / correction / epilogue — thread t owns row t (TMEM lane t):
-//             tcgen05.ld S row, online softmax in base 2 (scale*log2 e folded),
-//             lazy warp-uniform O rescale in TMEM, P (bf16, 128B-swizzled) to smem,
-//             final O / l -> bf16 -> global.
-// The S MMA of tile j+1 overlaps the softmax of tile j; the P.V MMA of tile j
-// overlaps the softmax of tile j+1.
+// B200 design — one CTA per (128-row q tile, head, sequence), TWO CTAs per SM:
+//   * smem: Q, K, V tiles only (single-buffered, 128B-swizzled, TMA-fed; 96 KiB
+//     at head_dim 128), TMEM: 256 columns = S/P (128) + O (128). Two co-resident
+//     CTAs interleave their softmax and MMA phases (ping-pong across CTAs), and
+//     one CTA's prologue/epilogue overlaps the other's main loop.
+//   * warp 4  TMA producer: Q once; K_j as soon as S_{j-1} has consumed K; V_j
+//             as soon as P_{j-1}V_{j-1} has consumed V. Afterwards it writes the
+//             diagonal K/V tile (the only one this CTA owns) to the paged cache
+//             with TMA tensor stores, one 16-token page per store (a3 fused).
+//   * warp 5  MMA issuer (one elected lane): S_j = Q K_j^T (SS, fp32 in TMEM);
+//             O += P_j V_j (TS: P read from TMEM, V MN-major from smem).
+//   * warps 0-3 softmax: thread t owns q row t (TMEM lane t): tcgen05.ld S row,
+//             online base-2 softmax (scale*log2 e folded), P rounded to bf16 and
+//             written back over S in TMEM (tcgen05.st), lazy warp-uniform O
+//             rescale in TMEM, final O / l -> bf16 -> global.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -28,27 +29,27 @@ namespace {
 
 constexpr int kBM = 128, kBN = 128;
 constexpr int kThreads = 192;
-constexpr uint32_t kChunkBytes = 128 * 128;  // 128 rows x 128 B (64 bf16) swizzle atom column
+constexpr uint32_t kChunkBytes = 128 * 128;  // 128 rows x 128 B (64 bf16): one SW128 column block
+constexpr uint32_t kTmemCols = 256;          // S/P [0,128) + O [128, 128+D)
 
 template <int D>
 struct Smem {
   static constexpr uint32_t kTile = kBM * D * 2;  // one Q/K/V tile
   static constexpr uint32_t Q = 0;
-  static constexpr uint32_t K0 = Q + kTile;
-  static constexpr uint32_t V0 = K0 + 2 * kTile;
-  static constexpr uint32_t P = V0 + 2 * kTile;
-  static constexpr uint32_t BAR = P + kBM * kBN * 2;
-  static constexpr uint32_t kBars = 12;
+  static constexpr uint32_t K = Q + kTile;
+  static constexpr uint32_t V = K + kTile;
+  static constexpr uint32_t BAR = V + kTile;
+  static constexpr uint32_t kBars = 8;
   static constexpr uint32_t TMEM_SLOT = BAR + kBars * 8;
   static constexpr uint32_t TOTAL = TMEM_SLOT + 16;
   static constexpr uint32_t ALLOC = TOTAL + 1024;  // slack for 1024-B alignment
 };
 
 // barrier indices
-enum { B_Q = 0, B_K0, B_K1, B_V0, B_V1, B_E0, B_E1, B_S0, B_S1, B_P, B_O };
+enum { B_Q = 0, B_KF, B_VF, B_KE, B_VE, B_S, B_P, B_O };
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v,
                    const __grid_constant__ CUtensorMap tm_cache, const PrefillArgs a) {
@@ -72,18 +73,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
 
   if (threadIdx.x == 0) {
-    for (int b = B_Q; b <= B_O; ++b) mbar_init(&bars[b], b == B_P ? 128 : 1);
+    for (int b = 0; b < (int)S::kBars; ++b) mbar_init(&bars[b], b == B_P ? 128 : 1);
     fence_barrier_init();
   }
   if (warp == 5) {
-    tmem_alloc<512>(tmem_slot);
+    tmem_alloc<kTmemCols>(tmem_slot);
     tmem_relinquish();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tO = tmem + 256;
+  const uint32_t tS = tmem, tO = tmem + kBN;
 
   if (warp == 4) {
     // ------------------------------------------------------------ producer
@@ -92,43 +93,37 @@ __global__ void __launch_bounds__(kThreads, 1)
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_cache);
-      const int q_row0 = seq_start + i * kBM;
+      const int row0 = seq_start + i * kBM;
       mbar_arrive_expect_tx(&bars[B_Q], S::kTile);
 #pragma unroll
       for (int c = 0; c < kChunks; ++c)
-        tma_load_3d(smem + S::Q + c * kChunkBytes, &tm_q, &bars[B_Q], c * 64, h, q_row0);
+        tma_load_3d(smem + S::Q + c * kChunkBytes, &tm_q, &bars[B_Q], c * 64, h, row0);
       for (int j = 0; j < ntiles; ++j) {
-        const int st = j & 1;
-        if (j >= 2) mbar_wait(&bars[B_E0 + st], ((j >> 1) - 1) & 1);
-        const int kv_row0 = seq_start + j * kBN;
-        mbar_arrive_expect_tx(&bars[B_K0 + st], S::kTile);
+        const int kv0 = seq_start + j * kBN;
+        if (j > 0) mbar_wait(&bars[B_KE], (j - 1) & 1);  // S_{j-1} has consumed K
+        mbar_arrive_expect_tx(&bars[B_KF], S::kTile);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c)
-          tma_load_3d(smem + S::K0 + st * S::kTile + c * kChunkBytes, &tm_k, &bars[B_K0 + st],
-                      c * 64, h, kv_row0);
-        mbar_arrive_expect_tx(&bars[B_V0 + st], S::kTile);
+          tma_load_3d(smem + S::K + c * kChunkBytes, &tm_k, &bars[B_KF], c * 64, h, kv0);
+        if (j > 0) mbar_wait(&bars[B_VE], (j - 1) & 1);  // P_{j-1} V_{j-1} has consumed V
+        mbar_arrive_expect_tx(&bars[B_VF], S::kTile);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c)
-          tma_load_3d(smem + S::V0 + st * S::kTile + c * kChunkBytes, &tm_v, &bars[B_V0 + st],
-                      c * 64, h, kv_row0);
+          tma_load_3d(smem + S::V + c * kChunkBytes, &tm_v, &bars[B_VF], c * 64, h, kv0);
       }
-      // a3: the diagonal K/V tile (j == i) -> paged cache, one 16-token page per store.
-      const int st = i & 1;
-      mbar_wait(&bars[B_K0 + st], (i >> 1) & 1);
-      mbar_wait(&bars[B_V0 + st], (i >> 1) & 1);
-      const int rem = len - i * kBM;
-      const int npg = min(8, (rem + 15) >> 4);
+      // a3: the diagonal K/V tile (j == i, the last one loaded) -> paged cache
+      mbar_wait(&bars[B_KF], (ntiles - 1) & 1);
+      mbar_wait(&bars[B_VF], (ntiles - 1) & 1);
+      const int npg = min(8, (len - i * kBM + 15) >> 4);
       const int32_t *bt = a.block_table + (size_t)r * a.max_blocks + i * 8;
       for (int p = 0; p < npg; ++p) {
         const int blk = bt[p];
 #pragma unroll
-        for (int kv = 0; kv < 2; ++kv) {
-          const uint8_t *tile = smem + (kv ? S::V0 : S::K0) + st * S::kTile;
+        for (int kv = 0; kv < 2; ++kv)
 #pragma unroll
           for (int c = 0; c < kChunks; ++c)
-            tma_store_4d(&tm_cache, tile + c * kChunkBytes + p * 16 * 128, c * 64, 0, h,
+            tma_store_4d(&tm_cache, smem + (kv ? S::V : S::K) + c * kChunkBytes + p * 16 * 128, c * 64, 0, h,
                          (a.layer * 2 + kv) * a.num_blocks + blk);
-        }
       }
       bulk_commit_group();
       bulk_wait_group_read0();
@@ -140,37 +135,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, D, 0, 1);
       mbar_wait(&bars[B_Q], 0);
-      tc_fence_after();
-      for (int j = 0; j <= ntiles; ++j) {
-        if (j < ntiles) {
-          const int st = j & 1;
-          mbar_wait(&bars[B_K0 + st], (j >> 1) & 1);
-          tc_fence_after();
+      for (int j = 0; j < ntiles; ++j) {
+        mbar_wait(&bars[B_KF], j & 1);
+        if (j > 0) mbar_wait(&bars[B_O], (j - 1) & 1);  // P_{j-1} (aliasing S) has been consumed
+        tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kChunkBytes + (kk & 3) * 32;
-            const uint64_t da = smem_desc_sw128(sbase + S::Q + off, 16, 1024);
-            const uint64_t db = smem_desc_sw128(sbase + S::K0 + st * S::kTile + off, 16, 1024);
-            umma_ss(tmem + st * kBN, da, db, idesc_s, kk > 0);
-          }
-          umma_commit(&bars[B_S0 + st]);
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kChunkBytes + (kk & 3) * 32;
+          umma_ss(tS, smem_desc_sw128(sbase + S::Q + off, 16, 1024),
+                  smem_desc_sw128(sbase + S::K + off, 16, 1024), idesc_s, kk > 0);
         }
-        if (j >= 1) {
-          const int jj = j - 1, st = jj & 1;
-          mbar_wait(&bars[B_P], jj & 1);
-          mbar_wait(&bars[B_V0 + st], (jj >> 1) & 1);
-          tc_fence_after();
+        umma_commit(&bars[B_S]);
+        umma_commit(&bars[B_KE]);
+        mbar_wait(&bars[B_P], j & 1);
+        mbar_wait(&bars[B_VF], j & 1);
+        tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk) {
-            const uint64_t da =
-                smem_desc_sw128(sbase + S::P + (kk >> 2) * kChunkBytes + (kk & 3) * 32, 16, 1024);
-            const uint64_t db =
-                smem_desc_sw128(sbase + S::V0 + st * S::kTile + kk * 16 * 128, kChunkBytes, 1024);
-            umma_ss(tO, da, db, idesc_o, (jj > 0 || kk > 0));
-          }
-          umma_commit(&bars[B_O]);
-          umma_commit(&bars[B_E0 + st]);
-        }
+        for (int kk = 0; kk < kBN / 16; ++kk)  // P: 16 kv columns = 8 packed TMEM columns per step
+          umma_ts(tO, tS + kk * 8, smem_desc_sw128(sbase + S::V + kk * 16 * 128, kChunkBytes, 1024),
+                  idesc_o, (j > 0 || kk > 0));
+        umma_commit(&bars[B_O]);
+        umma_commit(&bars[B_VE]);
       }
     }
     __syncwarp();
@@ -180,14 +165,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     const float sl2 = a.scale_log2;
     float m = -__int_as_float(0x7f800000), l = 0.f;
-    uint8_t *prow = smem + S::P + row * 128;
     for (int j = 0; j < ntiles; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&bars[B_S0 + sb], (j >> 1) & 1);
+      mbar_wait(&bars[B_S], j & 1);  // also implies P_{j-1} V_{j-1} finished (issued before S_j)
       tc_fence_after();
       uint32_t sr[4][32];
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) tmem_ld32(tmem + lane_off + sb * kBN + cc * 32, sr[cc]);
+      for (int cc = 0; cc < 4; ++cc) tmem_ld32(tS + lane_off + cc * 32, sr[cc]);
       tmem_wait_ld();
       const bool diag = (j == i);
       float mx = -__int_as_float(0x7f800000);
@@ -204,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float alpha = ex2(m - m_new);
       // p = 2^(x - m) rounded to bf16 (the P operand of the P.V MMA); the row sum
       // is taken over the same rounded values so numerator and normaliser agree.
-      uint32_t pk[64];
+      uint32_t pk[2][32];
       float rs = 0.f;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc)
@@ -213,37 +196,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t pr = pack_bf16(ex2(__uint_as_float(sr[cc][e]) - m_new),
                                         ex2(__uint_as_float(sr[cc][e + 1]) - m_new));
           rs += bf16lo(pr) + bf16hi(pr);
-          pk[cc * 16 + e / 2] = pr;
+          pk[cc >> 1][(cc & 1) * 16 + e / 2] = pr;
         }
       l = l * alpha + rs;
       m = m_new;
-      if (j > 0) {
-        // P smem and O are in use by P_{j-1} V_{j-1}: wait for it
-        mbar_wait(&bars[B_O], (j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha < 1.f)) {
+      if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {  // lazy, warp-uniform O rescale
 #pragma unroll
-          for (int cc = 0; cc < D / 32; ++cc) {
-            uint32_t o[32];
-            tmem_ld32(tO + lane_off + cc * 32, o);
-            tmem_wait_ld();
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t o[32];
+          tmem_ld32(tO + lane_off + cc * 32, o);
+          tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st32(tO + lane_off + cc * 32, o);
-          }
-          tmem_wait_st();
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tmem_st32(tO + lane_off + cc * 32, o);
         }
       }
-      // P row -> smem, K-major SWIZZLE_128B: 16-B piece pc of chunk c2 at pc ^ (row & 7)
-#pragma unroll
-      for (int c2 = 0; c2 < 2; ++c2)
-#pragma unroll
-        for (int pc = 0; pc < 8; ++pc) {
-          const int w0 = c2 * 32 + pc * 4;
-          const uint4 v = make_uint4(pk[w0], pk[w0 + 1], pk[w0 + 2], pk[w0 + 3]);
-          *reinterpret_cast<uint4 *>(prow + c2 * kChunkBytes + ((pc ^ (row & 7)) << 4)) = v;
-        }
-      fence_proxy_async_smem();
+      // P (bf16 pairs, low half = even kv column) over the first 64 columns of S
+      tmem_st32(tS + lane_off + 0, pk[0]);
+      tmem_st32(tS + lane_off + 32, pk[1]);
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bars[B_P]);
     }
@@ -252,8 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const float inv_l = 1.f / l;
     const int q_pos = i * kBM + row;
-    uint16_t *orow = reinterpret_cast<uint16_t *>(a.out) +
-                     ((size_t)(seq_start + q_pos) * a.n_loc + h) * D;
+    uint16_t *orow = reinterpret_cast<uint16_t *>(a.out) + ((size_t)(seq_start + q_pos) * a.n_loc + h) * D;
 #pragma unroll
     for (int cc = 0; cc < D / 32; ++cc) {
       uint32_t o[32];
@@ -277,14 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 5) {
     tc_fence_after();
-    tmem_dealloc<512>(tmem);
+    tmem_dealloc<kTmemCols>(tmem);
   }
-}
-
-}  // namespace
-
-size_t prefill_smem_bytes(int head_dim) {
-  return head_dim == 128 ? Smem<128>::ALLOC : Smem<64>::ALLOC;
 }
 
 template <int D>
@@ -292,6 +256,12 @@ static cudaError_t set_prefill_smem_once() {
   static cudaError_t st = cudaFuncSetAttribute(prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)Smem<D>::ALLOC);
   return st;
+}
+
+}  // namespace
+
+size_t prefill_smem_bytes(int head_dim) {
+  return head_dim == 128 ? Smem<128>::ALLOC : Smem<64>::ALLOC;
 }
 
 cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
