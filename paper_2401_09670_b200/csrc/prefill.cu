@@ -172,33 +172,40 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) tmem_ld32(tS + lane_off + cc * 32, sr[cc]);
       tmem_wait_ld();
-      const bool diag = (j == i);
+      // row max on the raw scores (scale > 0 preserves order); only the diagonal
+      // tile is masked (key column > query row)
       float mx = -__int_as_float(0x7f800000);
+      if (j == i) {
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc)
+        for (int cc = 0; cc < 4; ++cc)
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          float x = __uint_as_float(sr[cc][e]) * sl2;
-          if (diag && (cc * 32 + e) > row) x = -__int_as_float(0x7f800000);
-          sr[cc][e] = __float_as_uint(x);
-          mx = fmaxf(mx, x);
-        }
-      const float m_new = fmaxf(m, mx);
+          for (int e = 0; e < 32; ++e) {
+            if (cc * 32 + e > row) sr[cc][e] = 0xff800000u;  // -inf
+            mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
+          }
+      } else {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
+      }
+      const float m_new = fmaxf(m, mx * sl2);  // running max in the scaled base-2 domain
       const float alpha = ex2(m - m_new);
-      // p = 2^(x - m) rounded to bf16 (the P operand of the P.V MMA); the row sum
-      // is taken over the same rounded values so numerator and normaliser agree.
+      // p = 2^(s*scale*log2e - m): one FFMA + one MUFU ex2 per element; P is
+      // rounded to bf16 (the P operand of the P.V MMA), the row sum stays fp32.
       uint32_t pk[2][32];
-      float rs = 0.f;
+      float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc)
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const uint32_t pr = pack_bf16(ex2(__uint_as_float(sr[cc][e]) - m_new),
-                                        ex2(__uint_as_float(sr[cc][e + 1]) - m_new));
-          rs += bf16lo(pr) + bf16hi(pr);
-          pk[cc >> 1][(cc & 1) * 16 + e / 2] = pr;
+          const float p0 = ex2(fmaf(__uint_as_float(sr[cc][e]), sl2, -m_new));
+          const float p1 = ex2(fmaf(__uint_as_float(sr[cc][e + 1]), sl2, -m_new));
+          rs0 += p0;
+          rs1 += p1;
+          pk[cc >> 1][(cc & 1) * 16 + e / 2] = pack_bf16(p0, p1);
         }
-      l = l * alpha + rs;
+      l = l * alpha + (rs0 + rs1);
       m = m_new;
       if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {  // lazy, warp-uniform O rescale
 #pragma unroll
