@@ -93,11 +93,11 @@ static ds_status encode(CUtensorMap *m, void *base, int rank, const cuuint64_t *
   return DS_OK;
 }
 
-// [T][n][D] token-major activations, box = 128 rows x 64 dims of one head
-static ds_status qkv_map(CUtensorMap *m, const void *p, int T, int n, int D, const char *where) {
+// [T][n][D] token-major activations, box = `rows` tokens x 64 dims of one head
+static ds_status qkv_map(CUtensorMap *m, const void *p, int T, int n, int D, int rows, const char *where) {
   const cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)n, (cuuint64_t)T};
   const cuuint64_t str[2] = {(cuuint64_t)D * 2, (cuuint64_t)n * D * 2};
-  const cuuint32_t box[3] = {64, 1, 128};
+  const cuuint32_t box[3] = {64, 1, (cuuint32_t)rows};
   return encode(m, const_cast<void *>(p), 3, dims, str, box, where);
 }
 
@@ -150,9 +150,9 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
   if (ds_status s = require_sm100(W)) return s;
   const int D = cache->head_dim, n = cache->num_heads;
   CUtensorMap tq, tk, tv, tc;
-  if (ds_status s = qkv_map(&tq, q, total_tokens, n, D, W)) return s;
-  if (ds_status s = qkv_map(&tk, k, total_tokens, n, D, W)) return s;
-  if (ds_status s = qkv_map(&tv, v, total_tokens, n, D, W)) return s;
+  if (ds_status s = qkv_map(&tq, q, total_tokens, n, D, kPrefillQRows, W)) return s;
+  if (ds_status s = qkv_map(&tk, k, total_tokens, n, D, kPrefillKVRows, W)) return s;
+  if (ds_status s = qkv_map(&tv, v, total_tokens, n, D, kPrefillKVRows, W)) return s;
   if (ds_status s = cache_map(&tc, cache, W)) return s;
   PrefillArgs a{};
   a.out = out;

@@ -48,6 +48,8 @@ struct KvLocalArgs {
 cudaError_t launch_kv_local(const KvLocalArgs &a, cudaStream_t stream);
 
 // a2 + a3
+constexpr int kPrefillQRows = 128;  // q rows per CTA (TMA box of Q)
+constexpr int kPrefillKVRows = 64;  // keys per kv tile (TMA box of K and V)
 struct PrefillArgs {
   void *out;                   // bf16 [T][n][D]
   const int32_t *cu_seqlens;   // [B+1]

@@ -7,52 +7,59 @@
 //   cache[layer][K|V][bt[r][t/16]][h][t%16] = k|v[t][h]       (a3)
 //
 // B200 design — one CTA per (128-row q tile, head, sequence), TWO CTAs per SM:
-//   * smem: Q, K, V tiles only (single-buffered, 128B-swizzled, TMA-fed; 96 KiB
-//     at head_dim 128), TMEM: 256 columns = S/P (128) + O (128). Two co-resident
-//     CTAs interleave their softmax and MMA phases (ping-pong across CTAs), and
-//     one CTA's prologue/epilogue overlaps the other's main loop.
-//   * warp 4  TMA producer: Q once; K_j as soon as S_{j-1} has consumed K; V_j
-//             as soon as P_{j-1}V_{j-1} has consumed V. Afterwards it writes the
-//             diagonal K/V tile (the only one this CTA owns) to the paged cache
-//             with TMA tensor stores, one 16-token page per store (a3 fused).
-//   * warp 5  MMA issuer (one elected lane): S_j = Q K_j^T (SS, fp32 in TMEM);
-//             O += P_j V_j (TS: P read from TMEM, V MN-major from smem).
+//   * kv tiles of 64 keys: smem holds Q (32 KiB) + 2 K stages + 2 V stages
+//     (4 x 16 KiB, 128B-swizzled, TMA-fed) = 96 KiB at head_dim 128; TMEM holds
+//     256 columns = S0 | S1 (64 fp32 columns each, double-buffered) | O (128).
+//     N = 64 MMAs run at the same per-MAC rate as N = 128; the 64-key tiles buy
+//     double buffering of K, V and S inside the 2-CTA/SM budget, so S_{j+1}
+//     and the K/V loads of tile j+1 overlap the softmax of tile j, and the two
+//     co-resident CTAs interleave their softmax and MMA phases.
+//   * warp 4  TMA producer: Q once; K_j / V_j into stage j%2 as soon as S_{j-2}
+//             / P_{j-2}V_{j-2} released it. Afterwards it writes the two
+//             diagonal K/V tiles (the only ones this CTA owns) to the paged
+//             cache with TMA tensor stores, one 16-token page per store (a3).
+//   * warp 5  MMA issuer (one elected lane): S_j = Q K_j^T (SS, fp32 in TMEM
+//             buffer j%2), then O += P_{j-1} V_{j-1} (TS: P read from TMEM, V
+//             MN-major from smem).
 //   * warps 0-3 softmax: thread t owns q row t (TMEM lane t): tcgen05.ld S row,
-//             online base-2 softmax (scale*log2 e folded), P rounded to bf16 and
-//             written back over S in TMEM (tcgen05.st), lazy warp-uniform O
-//             rescale in TMEM, final O / l -> bf16 -> global.
+//             online base-2 softmax (scale*log2 e folded into one FFMA), P
+//             rounded to bf16 and written back over its S buffer in TMEM
+//             (tcgen05.st), lazy warp-uniform O rescale in TMEM, final
+//             O / l -> bf16 -> global.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ds {
 namespace {
 
-constexpr int kBM = 128, kBN = 128;
+constexpr int kBM = 128, kBN = 64;  // q rows per CTA, keys per kv tile
 constexpr int kThreads = 192;
-constexpr uint32_t kChunkBytes = 128 * 128;  // 128 rows x 128 B (64 bf16): one SW128 column block
-constexpr uint32_t kTmemCols = 256;          // S/P [0,128) + O [128, 128+D)
+constexpr uint32_t kChunkBytes128 = 128 * 128;  // Q: 128 rows x 128 B (64 bf16) per SW128 column block
+constexpr uint32_t kChunkBytes64 = 64 * 128;    // K/V tile: 64 rows x 128 B per SW128 column block
+constexpr uint32_t kTmemCols = 256;             // S0 [0,64) S1 [64,128) O [128, 128+D)
 
 template <int D>
 struct Smem {
-  static constexpr uint32_t kTile = kBM * D * 2;  // one Q/K/V tile
+  static constexpr uint32_t kQTile = kBM * D * 2;
+  static constexpr uint32_t kKVTile = kBN * D * 2;
   static constexpr uint32_t Q = 0;
-  static constexpr uint32_t K = Q + kTile;
-  static constexpr uint32_t V = K + kTile;
-  static constexpr uint32_t BAR = V + kTile;
-  static constexpr uint32_t kBars = 8;
+  static constexpr uint32_t K0 = Q + kQTile;           // 2 stages
+  static constexpr uint32_t V0 = K0 + 2 * kKVTile;     // 2 stages
+  static constexpr uint32_t BAR = V0 + 2 * kKVTile;
+  static constexpr uint32_t kBars = 14;
   static constexpr uint32_t TMEM_SLOT = BAR + kBars * 8;
   static constexpr uint32_t TOTAL = TMEM_SLOT + 16;
   static constexpr uint32_t ALLOC = TOTAL + 1024;  // slack for 1024-B alignment
 };
 
-// barrier indices
-enum { B_Q = 0, B_KF, B_VF, B_KE, B_VE, B_S, B_P, B_O };
+// barrier indices ([2] = per stage / per S buffer)
+enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_P = 11, B_O = 12 };
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 2)
-    prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                   const __grid_constant__ CUtensorMap tm_v,
-                   const __grid_constant__ CUtensorMap tm_cache, const PrefillArgs a) {
+    prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
+                   const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_cache,
+                   const PrefillArgs a) {
   using S = Smem<D>;
   constexpr int kChunks = D / 64;
   // q tiles of one (sequence, head) are adjacent in launch order so their K/V
@@ -62,7 +69,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int seq_start = a.cu_seqlens[r];
   const int len = a.cu_seqlens[r + 1] - seq_start;
   if (i * kBM >= len) return;
-  const int ntiles = i + 1;
+  // kv tiles 0 .. 2i+1 (64 keys each); the second diagonal tile is skipped when
+  // it lies wholly past the end of the sequence
+  const int ntiles = 2 * i + 1 + (len - i * kBM > kBN ? 1 : 0);
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -84,46 +93,49 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS = tmem, tO = tmem + kBN;
+  const uint32_t tO = tmem + 128;
 
   if (warp == 4) {
     // ------------------------------------------------------------ producer
     if (elect_one()) {
       tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_kv);
       tma_prefetch_desc(&tm_v);
       tma_prefetch_desc(&tm_cache);
-      const int row0 = seq_start + i * kBM;
-      mbar_arrive_expect_tx(&bars[B_Q], S::kTile);
+      mbar_arrive_expect_tx(&bars[B_Q], S::kQTile);
 #pragma unroll
       for (int c = 0; c < kChunks; ++c)
-        tma_load_3d(smem + S::Q + c * kChunkBytes, &tm_q, &bars[B_Q], c * 64, h, row0);
+        tma_load_3d(smem + S::Q + c * kChunkBytes128, &tm_q, &bars[B_Q], c * 64, h, seq_start + i * kBM);
       for (int j = 0; j < ntiles; ++j) {
-        const int kv0 = seq_start + j * kBN;
-        if (j > 0) mbar_wait(&bars[B_KE], (j - 1) & 1);  // S_{j-1} has consumed K
-        mbar_arrive_expect_tx(&bars[B_KF], S::kTile);
+        const int st = j & 1, kv0 = seq_start + j * kBN;
+        if (j >= 2) mbar_wait(&bars[B_KE + st], ((j >> 1) - 1) & 1);  // S_{j-2} has consumed K stage
+        mbar_arrive_expect_tx(&bars[B_KF + st], S::kKVTile);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c)
-          tma_load_3d(smem + S::K + c * kChunkBytes, &tm_k, &bars[B_KF], c * 64, h, kv0);
-        if (j > 0) mbar_wait(&bars[B_VE], (j - 1) & 1);  // P_{j-1} V_{j-1} has consumed V
-        mbar_arrive_expect_tx(&bars[B_VF], S::kTile);
+          tma_load_3d(smem + S::K0 + st * S::kKVTile + c * kChunkBytes64, &tm_kv, &bars[B_KF + st], c * 64, h, kv0);
+        if (j >= 2) mbar_wait(&bars[B_VE + st], ((j >> 1) - 1) & 1);  // PV_{j-2} has consumed V stage
+        mbar_arrive_expect_tx(&bars[B_VF + st], S::kKVTile);
 #pragma unroll
         for (int c = 0; c < kChunks; ++c)
-          tma_load_3d(smem + S::V + c * kChunkBytes, &tm_v, &bars[B_VF], c * 64, h, kv0);
+          tma_load_3d(smem + S::V0 + st * S::kKVTile + c * kChunkBytes64, &tm_v, &bars[B_VF + st], c * 64, h, kv0);
       }
-      // a3: the diagonal K/V tile (j == i, the last one loaded) -> paged cache
-      mbar_wait(&bars[B_KF], (ntiles - 1) & 1);
-      mbar_wait(&bars[B_VF], (ntiles - 1) & 1);
+      // a3: the diagonal K/V tiles 2i (pages 8i..8i+3) and 2i+1 (8i+4..8i+7) -> paged cache
       const int npg = min(8, (len - i * kBM + 15) >> 4);
       const int32_t *bt = a.block_table + (size_t)r * a.max_blocks + i * 8;
-      for (int p = 0; p < npg; ++p) {
-        const int blk = bt[p];
+      for (int t = 2 * i; t < ntiles; ++t) {
+        const int st = t & 1;
+        mbar_wait(&bars[B_KF + st], (t >> 1) & 1);
+        mbar_wait(&bars[B_VF + st], (t >> 1) & 1);
+        for (int p = (t - 2 * i) * 4; p < min(npg, (t - 2 * i) * 4 + 4); ++p) {
+          const int blk = bt[p];
 #pragma unroll
-        for (int kv = 0; kv < 2; ++kv)
+          for (int kv = 0; kv < 2; ++kv)
 #pragma unroll
-          for (int c = 0; c < kChunks; ++c)
-            tma_store_4d(&tm_cache, smem + (kv ? S::V : S::K) + c * kChunkBytes + p * 16 * 128, c * 64, 0, h,
-                         (a.layer * 2 + kv) * a.num_blocks + blk);
+            for (int c = 0; c < kChunks; ++c)
+              tma_store_4d(&tm_cache,
+                           smem + (kv ? S::V0 : S::K0) + st * S::kKVTile + c * kChunkBytes64 + (p & 3) * 16 * 128,
+                           c * 64, 0, h, (a.layer * 2 + kv) * a.num_blocks + blk);
+        }
       }
       bulk_commit_group();
       bulk_wait_group_read0();
@@ -135,57 +147,67 @@ __global__ void __launch_bounds__(kThreads, 2)
       constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, D, 0, 1);
       mbar_wait(&bars[B_Q], 0);
-      for (int j = 0; j < ntiles; ++j) {
-        mbar_wait(&bars[B_KF], j & 1);
-        if (j > 0) mbar_wait(&bars[B_O], (j - 1) & 1);  // P_{j-1} (aliasing S) has been consumed
+      auto issue_pv = [&](int jj) {  // O += P_jj V_jj
+        const int st = jj & 1;
+        mbar_wait(&bars[B_P], jj & 1);
+        mbar_wait(&bars[B_VF + st], (jj >> 1) & 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * kChunkBytes + (kk & 3) * 32;
-          umma_ss(tS, smem_desc_sw128(sbase + S::Q + off, 16, 1024),
-                  smem_desc_sw128(sbase + S::K + off, 16, 1024), idesc_s, kk > 0);
-        }
-        umma_commit(&bars[B_S]);
-        umma_commit(&bars[B_KE]);
-        mbar_wait(&bars[B_P], j & 1);
-        mbar_wait(&bars[B_VF], j & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)  // P: 16 kv columns = 8 packed TMEM columns per step
-          umma_ts(tO, tS + kk * 8, smem_desc_sw128(sbase + S::V + kk * 16 * 128, kChunkBytes, 1024),
-                  idesc_o, (j > 0 || kk > 0));
+        for (int kk = 0; kk < kBN / 16; ++kk)  // 16 keys = 8 packed P columns per step
+          umma_ts(tO, tmem + st * kBN + kk * 8,
+                  smem_desc_sw128(sbase + S::V0 + st * S::kKVTile + kk * 16 * 128, kChunkBytes64, 1024), idesc_o,
+                  (jj > 0 || kk > 0));
         umma_commit(&bars[B_O]);
-        umma_commit(&bars[B_VE]);
+        umma_commit(&bars[B_VE + st]);
+      };
+      for (int j = 0; j < ntiles; ++j) {
+        const int st = j & 1;
+        mbar_wait(&bars[B_KF + st], (j >> 1) & 1);
+        if (j >= 2) mbar_wait(&bars[B_O], (j - 2) & 1);  // P_{j-2} (aliasing S buffer st) consumed
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          umma_ss(tmem + st * kBN, smem_desc_sw128(sbase + S::Q + (kk >> 2) * kChunkBytes128 + (kk & 3) * 32, 16, 1024),
+                  smem_desc_sw128(sbase + S::K0 + st * S::kKVTile + (kk >> 2) * kChunkBytes64 + (kk & 3) * 32, 16,
+                                  1024),
+                  idesc_s, kk > 0);
+        umma_commit(&bars[B_SF + st]);
+        umma_commit(&bars[B_KE + st]);
+        if (j >= 1) issue_pv(j - 1);
       }
+      issue_pv(ntiles - 1);
     }
     __syncwarp();
   } else {
     // ------------------------------------------------------------ softmax warps 0-3
     const int row = threadIdx.x;  // TMEM lane == q row within the tile
+    const int q_pos = i * kBM + row;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
     const float sl2 = a.scale_log2;
     float m = -__int_as_float(0x7f800000), l = 0.f;
     for (int j = 0; j < ntiles; ++j) {
-      mbar_wait(&bars[B_S], j & 1);  // also implies P_{j-1} V_{j-1} finished (issued before S_j)
+      const int st = j & 1;
+      mbar_wait(&bars[B_SF + st], (j >> 1) & 1);
       tc_fence_after();
-      uint32_t sr[4][32];
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) tmem_ld32(tS + lane_off + cc * 32, sr[cc]);
+      uint32_t sr[2][32];
+      tmem_ld32(tmem + lane_off + st * kBN, sr[0]);
+      tmem_ld32(tmem + lane_off + st * kBN + 32, sr[1]);
       tmem_wait_ld();
-      // row max on the raw scores (scale > 0 preserves order); only the diagonal
-      // tile is masked (key column > query row)
+      // row max on the raw scores (scale > 0 preserves order); only the two
+      // diagonal tiles are masked (key position > query position)
       float mx = -__int_as_float(0x7f800000);
-      if (j == i) {
+      if (j >= 2 * i) {
+        const int kpos0 = j * kBN;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
+        for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            if (cc * 32 + e > row) sr[cc][e] = 0xff800000u;  // -inf
+            if (kpos0 + cc * 32 + e > q_pos) sr[cc][e] = 0xff800000u;  // -inf
             mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
           }
       } else {
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
+        for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
           for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
       }
@@ -193,34 +215,37 @@ __global__ void __launch_bounds__(kThreads, 2)
       const float alpha = ex2(m - m_new);
       // p = 2^(s*scale*log2e - m): one FFMA + one MUFU ex2 per element; P is
       // rounded to bf16 (the P operand of the P.V MMA), the row sum stays fp32.
-      uint32_t pk[2][32];
+      uint32_t pk[32];
       float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc)
+      for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           const float p0 = ex2(fmaf(__uint_as_float(sr[cc][e]), sl2, -m_new));
           const float p1 = ex2(fmaf(__uint_as_float(sr[cc][e + 1]), sl2, -m_new));
           rs0 += p0;
           rs1 += p1;
-          pk[cc >> 1][(cc & 1) * 16 + e / 2] = pack_bf16(p0, p1);
+          pk[cc * 16 + e / 2] = pack_bf16(p0, p1);
         }
       l = l * alpha + (rs0 + rs1);
       m = m_new;
-      if (j > 0 && __any_sync(0xffffffffu, alpha < 1.f)) {  // lazy, warp-uniform O rescale
+      if (j > 0) {
+        mbar_wait(&bars[B_O], (j - 1) & 1);  // O is not in use by P_{j-1} V_{j-1} any more
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha < 1.f)) {  // lazy, warp-uniform O rescale
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) {
-          uint32_t o[32];
-          tmem_ld32(tO + lane_off + cc * 32, o);
-          tmem_wait_ld();
+          for (int cc = 0; cc < D / 32; ++cc) {
+            uint32_t o[32];
+            tmem_ld32(tO + lane_off + cc * 32, o);
+            tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          tmem_st32(tO + lane_off + cc * 32, o);
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st32(tO + lane_off + cc * 32, o);
+          }
         }
       }
-      // P (bf16 pairs, low half = even kv column) over the first 64 columns of S
-      tmem_st32(tS + lane_off + 0, pk[0]);
-      tmem_st32(tS + lane_off + 32, pk[1]);
+      // P (bf16 pairs, low half = even key) over the first 32 columns of S buffer st
+      tmem_st32(tmem + lane_off + st * kBN, pk);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bars[B_P]);
@@ -229,7 +254,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_wait(&bars[B_O], (ntiles - 1) & 1);
     tc_fence_after();
     const float inv_l = 1.f / l;
-    const int q_pos = i * kBM + row;
     uint16_t *orow = reinterpret_cast<uint16_t *>(a.out) + ((size_t)(seq_start + q_pos) * a.n_loc + h) * D;
 #pragma unroll
     for (int cc = 0; cc < D / 32; ++cc) {
