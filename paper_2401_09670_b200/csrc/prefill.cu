@@ -37,6 +37,7 @@ constexpr int kThreads = 192;
 constexpr uint32_t kChunkBytes128 = 128 * 128;  // Q: 128 rows x 128 B (64 bf16) per SW128 column block
 constexpr uint32_t kChunkBytes64 = 64 * 128;    // K/V tile: 64 rows x 128 B per SW128 column block
 constexpr uint32_t kTmemCols = 256;             // S0 [0,64) S1 [64,128) O [128, 128+D)
+constexpr float kRescaleLog2 = 8.f;             // move the exponent base only past 2^8 growth
 
 template <int D>
 struct Smem {
@@ -211,8 +212,15 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
           for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
       }
-      const float m_new = fmaxf(m, mx * sl2);  // running max in the scaled base-2 domain
-      const float alpha = ex2(m - m_new);
+      // Conditional rescaling: the exponent base m only moves when this tile's
+      // row max exceeds it by more than kRescaleLog2 (p <= 2^8 in between, exact
+      // in fp32/bf16 range); softmax is invariant to the base, so the result is
+      // the same function — most tiles then skip the O rescale AND the wait on
+      // the previous P.V MMA.
+      const float m_tile = mx * sl2;
+      const bool grow = m_tile > m + kRescaleLog2;
+      const float m_new = grow ? m_tile : m;
+      const float alpha = grow ? ex2(m - m_new) : 1.f;
       // p = 2^(s*scale*log2e - m): one FFMA + one MUFU ex2 per element; P is
       // rounded to bf16 (the P operand of the P.V MMA), the row sum stays fp32.
       uint32_t pk[32];
@@ -229,19 +237,17 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       l = l * alpha + (rs0 + rs1);
       m = m_new;
-      if (j > 0) {
-        mbar_wait(&bars[B_O], (j - 1) & 1);  // O is not in use by P_{j-1} V_{j-1} any more
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {  // warp-uniform O rescale, only when a base moved
+        mbar_wait(&bars[B_O], (j - 1) & 1);          // O is not in use by P_{j-1} V_{j-1} any more
         tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha < 1.f)) {  // lazy, warp-uniform O rescale
 #pragma unroll
-          for (int cc = 0; cc < D / 32; ++cc) {
-            uint32_t o[32];
-            tmem_ld32(tO + lane_off + cc * 32, o);
-            tmem_wait_ld();
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t o[32];
+          tmem_ld32(tO + lane_off + cc * 32, o);
+          tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-            tmem_st32(tO + lane_off + cc * 32, o);
-          }
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          tmem_st32(tO + lane_off + cc * 32, o);
         }
       }
       // P (bf16 pairs, low half = even key) over the first 32 columns of S buffer st
