@@ -40,6 +40,22 @@ DS_DEVICE float ex2(float x) {
   return y;
 }
 
+// 2^x on the FMA pipe (offloads the MUFU unit, whose 16 ex2/clk/SM equal the
+// tensor pipe's demand in attention softmax). Cody-Waite split x = n + f with
+// n = rint(x) (magic-number add), f in [-0.5, 0.5], 2^f by a degree-3 minimax
+// polynomial (max relative error 1.4e-4, far below the bf16 rounding of P),
+// 2^n added straight into the exponent bits (one LEA). x <= 0 here; it is
+// clamped at -127 so -inf (masked keys) gives ~0.
+DS_DEVICE float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: rint(x) lands in the low mantissa bits
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(0x1.b6c8b8p-5f, f, 0x1.f06630p-3f);
+  p = fmaf(p, f, 0x1.631872p-1f);
+  p = fmaf(p, f, 0x1.fffa1ep-1f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 // ----------------------------------------------------------------- mbarrier
 DS_DEVICE void mbar_init(uint64_t *bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

@@ -229,8 +229,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(sr[cc][e]), sl2, -m_new));
-          const float p1 = ex2(fmaf(__uint_as_float(sr[cc][e + 1]), sl2, -m_new));
+          // 3 of every 8 exponentials on the FMA pipe, the rest on MUFU
+          const float x0 = fmaf(__uint_as_float(sr[cc][e]), sl2, -m_new);
+          const float x1 = fmaf(__uint_as_float(sr[cc][e + 1]), sl2, -m_new);
+          const float p0 = (e & 7) < 3 ? ex2_poly(x0) : ex2(x0);
+          const float p1 = ((e + 1) & 7) < 3 ? ex2_poly(x1) : ex2(x1);
           rs0 += p0;
           rs1 += p1;
           pk[cc * 16 + e / 2] = pack_bf16(p0, p1);
