@@ -44,10 +44,10 @@ DS_DEVICE float ex2(float x) {
 // tensor pipe's demand in attention softmax). Cody-Waite split x = n + f with
 // n = rint(x) (magic-number add), f in [-0.5, 0.5], 2^f by a degree-3 minimax
 // polynomial (max relative error 1.4e-4, far below the bf16 rounding of P),
-// 2^n added straight into the exponent bits (one LEA). x <= 0 here; it is
-// clamped at -127 so -inf (masked keys) gives ~0.
+// 2^n added straight into the exponent bits (one LEA). x is clamped at -126
+// (so -inf, a masked key, gives ~1e-38 and the exponent field cannot wrap).
 DS_DEVICE float ex2_poly(float x) {
-  x = fmaxf(x, -127.f);
+  x = fmaxf(x, -126.f);
   const float t = x + 12582912.f;  // 1.5 * 2^23: rint(x) lands in the low mantissa bits
   const float f = x - (t - 12582912.f);
   float p = fmaf(0x1.b6c8b8p-5f, f, 0x1.f06630p-3f);

@@ -38,6 +38,7 @@ constexpr uint32_t kChunkBytes128 = 128 * 128;  // Q: 128 rows x 128 B (64 bf16)
 constexpr uint32_t kChunkBytes64 = 64 * 128;    // K/V tile: 64 rows x 128 B per SW128 column block
 constexpr uint32_t kTmemCols = 256;             // S0 [0,64) S1 [64,128) O [128, 128+D)
 constexpr float kRescaleLog2 = 8.f;             // move the exponent base only past 2^8 growth
+constexpr int kPolyEvery = 8;                   // 1 in kPolyEvery exp2 on the FMA pipe (ex2_poly)
 
 template <int D>
 struct Smem {
@@ -229,11 +230,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          // 3 of every 8 exponentials on the FMA pipe, the rest on MUFU
+          // kPolyEvery-th exponentials on the FMA pipe, the rest on MUFU
           const float x0 = fmaf(__uint_as_float(sr[cc][e]), sl2, -m_new);
           const float x1 = fmaf(__uint_as_float(sr[cc][e + 1]), sl2, -m_new);
-          const float p0 = (e & 7) < 3 ? ex2_poly(x0) : ex2(x0);
-          const float p1 = ((e + 1) & 7) < 3 ? ex2_poly(x1) : ex2(x1);
+          const float p0 = (e % kPolyEvery) == 0 ? ex2_poly(x0) : ex2(x0);
+          const float p1 = ((e + 1) % kPolyEvery) == 0 ? ex2_poly(x1) : ex2(x1);
           rs0 += p0;
           rs1 += p1;
           pk[cc * 16 + e / 2] = pack_bf16(p0, p1);
