@@ -80,6 +80,20 @@ def parse():
     return p.parse_args()
 
 
+def ncu_traffic(args, w, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
+    of this configuration (profiles/<round>/ncu_traffic.json), else None."""
+    import glob
+    key = f"config{args.config}_B{w.B}"
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json")), reverse=True):
+        try:
+            d = json.load(open(path))[key][kernel]
+            return d["dram_read"] + d["dram_write"]
+        except Exception:
+            continue
+    return None
+
+
 def load_peaks():
     try:
         return json.load(open(PEAKS_PATH)), "measured"
@@ -543,11 +557,12 @@ def run_ds(args):
         comp["decode_attn_us_per_launch"] = avg_ms * 1e3
         comp["decode_graphs"] = eng.graphs is not None
     roofline = None  # the dominant kernel of this rank's step
+    traffic = ncu_traffic(args, w, "decode_kernel")
     if dec_kernel:
         achieved = dec_kernel[0] / (dec_kernel[1] / 1e3) / 1e9
         roofline = {"kernel": "ds_decode_attn (decode_kernel, split merge fused)", "bound": "hbm",
                     "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                    "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                     "algorithmic_bytes_per_launch": dec_kernel[0]}
     elif eng.pf:
