@@ -76,6 +76,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graphs", action="store_true", help="eager decode launches (no CUDA graphs)")
+    p.add_argument("--prefill-instances", type=int, default=0,
+                   help="N>1: prefill instances (0 = balance the phases with the roofline cost model)")
     p.add_argument("--profile", action="store_true", help="one short pass for ncu (no JSON)")
     return p.parse_args()
 
@@ -311,57 +313,83 @@ class Engine:
         torch.cuda.synchronize()
 
     # -- one step -------------------------------------------------------------------
-    def step(self, events=None):
-        ds, w, role = self.ds, self.w, self.role
-        ev = events or {}
-        if "start" in ev:
-            ev["start"].record()
-        if self.pf:  # a1 + a2/a3
-            tp = np.full((w.B, w.maxb), -1, np.int32)
-            ds.ds_block_table(self.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
-            tp_d = self.upload(tp)
-            for layer in range(w.L):
-                i = layer % len(self.q)
-                ds.ds_prefill_attn(self.q[i], self.k[i], self.v[i], self.out, self.cu, w.max_len,
-                                   self.P, layer, tp_d, w.scale)
-            self.launches += w.L
-            src_ids = self.page_ids(tp_d)
-        if "prefill_end" in ev:
-            ev["prefill_end"].record()
-        if self.dc:  # admission on the decode side (pull)
-            td = np.full((w.B, w.maxb), -1, np.int32)
-            ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, [0] * w.B, w.lens, td)
-            dst_ids = self.page_ids(self.upload(td))
-        # a4-a6
+    def _mark(self, marks, label):
+        if marks is not None:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record()
+            marks.append((label, e))
+
+    def prefill_and_send(self, peer, marks):
+        """a1 + a2/a3 for one batch, then a4-a6 towards decode rank `peer`."""
+        ds, w = self.ds, self.w
+        tp = np.full((w.B, w.maxb), -1, np.int32)
+        ds.ds_block_table(self.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
+        tp_d = self.upload(tp)
+        for layer in range(w.L):
+            i = layer % len(self.q)
+            ds.ds_prefill_attn(self.q[i], self.k[i], self.v[i], self.out, self.cu, w.max_len, self.P, layer, tp_d,
+                               w.scale)
+        self.launches += w.L
+        src_ids = self.page_ids(tp_d)
+        self._mark(marks, "prefill")
         if self.mrole == ds.DS_MIGRATE_LOCAL:
             ds.ds_kv_migrate(None, self.mrole, 0, self.P, 0, w.L, src_ids, 0, w.n, None,
-                             dst_cache=self.D, dst_block_ids=dst_ids)
+                             dst_cache=self.D, dst_block_ids=self.dst_ids)
             self.launches += 1
         else:
-            chunk_rows = max(1, (64 << 20) // (w.n * 16 * w.d * 2))
-            self.launches += -(-(2 * w.L * sum(w.pages)) // chunk_rows)  # pack or unpack kernels (+ NCCL's)
-            if self.pf:
-                ds.ds_kv_migrate(self.comm, self.mrole, role.peer, self.P, 0, w.L, src_ids, 0, w.n, self.staging)
+            ds.ds_kv_migrate(self.comm, self.mrole, peer, self.P, 0, w.L, src_ids, 0, w.n, self.staging)
+            self.launches += self.migrate_chunks()
+        # the pages are free again once the (stream-ordered) migration has read them
+        ds.ds_block_table(self.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
+        self._mark(marks, "migrate")
+
+    def migrate_chunks(self):
+        w = self.w
+        chunk_rows = max(1, (64 << 20) // (w.n * 16 * w.d * 2))
+        return -(-(2 * w.L * sum(w.pages)) // chunk_rows)  # pack or unpack kernels (+ NCCL's own)
+
+    def admit(self):
+        """decode-side admission of one batch (pull): pages for the prompts"""
+        ds, w = self.ds, self.w
+        self.td = np.full((w.B, w.maxb), -1, np.int32)
+        ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, [0] * w.B, w.lens, self.td)
+        self.dst_ids = self.page_ids(self.upload(self.td))
+
+    def decode_batch(self, marks):
+        """a1 (APPEND per step) + a7/a8 for `output` steps, then FREE"""
+        ds, w = self.ds, self.w
+        cur = list(w.lens)
+        for s in range(w.out_len):
+            ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, cur, [1] * w.B, self.td)
+            self.upload_decode(self.td, cur)
+            if self.graphs is not None:
+                self.graphs[s].replay()
             else:
-                ds.ds_kv_migrate(self.comm, self.mrole, role.peer, self.D, 0, w.L, dst_ids, 0, w.n, self.staging)
-        if self.pf:
-            ds.ds_block_table(self.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
-        if "migrate_end" in ev:
-            ev["migrate_end"].record()
-        if self.dc:  # a1 (APPEND per step) + a7/a8
-            cur = list(w.lens)
-            for s in range(w.out_len):
-                ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, cur, [1] * w.B, td)
-                self.upload_decode(td, cur)
-                if self.graphs is not None:
-                    self.graphs[s].replay()
-                else:
-                    self.decode_layers(s)
-                self.launches += w.L  # one decode_kernel per layer (split merge fused)
-                cur = [c + 1 for c in cur]
-            ds.ds_block_table(self.pool_d, ds.DS_BT_FREE, cur, None, td)
-        if "end" in ev:
-            ev["end"].record()
+                self.decode_layers(s)
+            self.launches += w.L  # one decode_kernel per layer (split merge fused)
+            cur = [c + 1 for c in cur]
+        ds.ds_block_table(self.pool_d, ds.DS_BT_FREE, cur, None, self.td)
+        self._mark(marks, "decode")
+
+    def step(self, marks=None):
+        """N=1: one batch through prefill -> LOCAL migrate -> decode.
+        prefill rank: one batch per decoding rank it feeds (round-robin dispatch).
+        decode rank: receive one batch, decode it."""
+        ds, w, role = self.ds, self.w, self.role
+        self._mark(marks, "start")
+        if role.phase == "both":
+            self.admit()
+            self.prefill_and_send(0, marks)
+            self.decode_batch(marks)
+        elif role.phase == "prefill":
+            for peer in role.peers:
+                self.prefill_and_send(peer, marks)
+        else:
+            self.admit()
+            ds.ds_kv_migrate(self.comm, self.mrole, role.peer, self.D, 0, w.L, self.dst_ids, 0, w.n, self.staging)
+            self.launches += self.migrate_chunks()
+            self._mark(marks, "migrate")
+            self.decode_batch(marks)
 
 
 # ----------------------------------------------------------------------------- distributed
@@ -434,21 +462,53 @@ def oracle_sample_tok_s(w: Workload, target_s: float = 15.0):
 
 
 # ----------------------------------------------------------------------------- arms
-def _config_line(w, world, replicas):
+def _config_line(w, world, replicas, roles=None):
     tp, pp = (1, 1) if world == 1 else (w.cfg["tp"], w.cfg["pp"])
+    n_p = 0 if world == 1 else sum(1 for r in roles if r.phase == "prefill") // (tp * pp)
     return {"workload": w.describe(), "batch": w.B, "prompt_tokens": w.T, "max_prompt": w.max_len,
-            "decode_steps": w.out_len, "mix": w.mix, "replicas": replicas, "tp": tp, "pp": pp,
+            "decode_steps": w.out_len, "mix": w.mix, "decode_instances": replicas, "prefill_instances": n_p,
+            "tp": tp, "pp": pp,
             "parallelism": "single GPU (P+D)" if world == 1 else
-            f"{replicas} replica pair(s) x TP{tp} PP{pp} prefill -> TP{tp} PP{pp} decode",
+            f"{n_p} prefill : {replicas} decode instances, TP{tp} PP{pp} each (round-robin dispatch)",
             "l2": "inputs larger than L2; no flush"}
 
 
-def _role_for(cfg, rank, world):
+def stage_costs(cfg, args):
+    """Roofline estimate (s) of one batch on a prefill rank (prefill + send) and on
+    a decoding rank (receive + decode) — the latency model that picks the split."""
     from paper_2401_09670_b200.pairing import assign
     g = cfg["geom"]
+    tp, pp = cfg["tp"], cfg["pp"]
+    role = assign(0, 2 * tp * pp, g.layers, g.heads, tp, pp)
+    w = Workload(cfg, args, role)
+    peaks, _ = load_peaks()
+    hbm, tc, nvl = 0.7 * peaks["hbm_gbs"] * 1e9, 0.5 * peaks["bf16_tflops"] * 1e12, 0.7 * NVLINK_GBS * 1e9
+    mig = w.kv_page_bytes() / nvl
+    t_p = w.L * max(w.prefill_flops_per_layer() / tc, w.prefill_bytes_per_layer() / hbm) + mig
+    t_d = sum(w.decode_bytes([c + s for c in w.lens]) for s in range(w.out_len)) * w.L / (0.85 * peaks["hbm_gbs"] * 1e9) + mig
+    return t_p, t_d
+
+
+def roles_for(cfg, world, args):
+    from paper_2401_09670_b200 import pairing
+    g = cfg["geom"]
     if world == 1:
-        return assign(0, 1, g.layers, g.heads)
-    return assign(rank, world, g.layers, g.heads, cfg["tp"], cfg["pp"])
+        return [pairing.assign(0, 1, g.layers, g.heads)]
+    tp, pp = cfg["tp"], cfg["pp"]
+    n_p = args.prefill_instances
+    if n_p <= 0:
+        t_p, t_d = stage_costs(cfg, args)
+        n_p = pairing.balanced_prefill_instances(world, tp, pp, t_p, t_d)
+    return pairing.all_roles(world, g.layers, g.heads, tp, pp, n_p)
+
+
+def _role_for(cfg, rank, world, args=None):
+    if args is None:
+        from paper_2401_09670_b200.pairing import assign
+        g = cfg["geom"]
+        return assign(0, 1, g.layers, g.heads) if world == 1 else \
+            assign(rank, world, g.layers, g.heads, cfg["tp"], cfg["pp"])
+    return roles_for(cfg, world, args)[rank]
 
 
 def run_reference(args):
@@ -480,14 +540,15 @@ def run_ds(args):
     import paper_2401_09670_b200 as ds
     from paper_2401_09670_b200 import pairing
     cfg = CONFIGS[args.config]
-    role = _role_for(cfg, rank, world)
+    roles = roles_for(cfg, world, args)
+    role = roles[rank]
     w = Workload(cfg, args, role)
     if world == 1:
         comm = None  # both instances on one GPU: LOCAL page copy, no communicator
     else:
         import torch.distributed as dist
         comm = ds.ds_comm_init(pairing.bootstrap_unique_id(ds.ds_comm_get_unique_id, rank, world, dist), world, rank)
-    replicas = 1 if world == 1 else world // 2 // (cfg["tp"] * cfg["pp"])
+    replicas = 1 if world == 1 else sum(1 for r in roles if r.phase == "decode") // (cfg["tp"] * cfg["pp"])
     eng = Engine(w, role, comm, seed=1234 + role.replica * 7919 + role.stage * 131 + role.tp_rank, torch=torch,
                  ds=ds)
     torch.cuda.synchronize()
@@ -513,31 +574,40 @@ def run_ds(args):
     torch.cuda.synchronize()
     t_start.record()
     for _ in range(args.steps):
-        evs = {k: torch.cuda.Event(enable_timing=True) for k in ("start", "prefill_end", "migrate_end", "end")}
-        eng.step(evs)
-        phase.append(evs)
+        marks = []
+        eng.step(marks)
+        phase.append(marks)
     t_end.record()
     torch.cuda.synchronize()
     barrier(world)
     clocks = sampler.stop()
     total_ms = max_over_ranks(t_start.elapsed_time(t_end), world)
     ms_step = total_ms / args.steps
-    value = replicas * (w.T + w.B * w.out_len) / (ms_step / 1e3)
+    n_dec = 1 if world == 1 else sum(1 for r in roles if r.phase == "decode") // (cfg["tp"] * cfg["pp"])
+    value = n_dec * (w.T + w.B * w.out_len) / (ms_step / 1e3)
 
     peaks, peak_kind = load_peaks()
     comp = {"phase": role.phase}
-    med = lambda a, b: statistics.median(e[a].elapsed_time(e[b]) for e in phase)  # noqa: E731
+
+    def phase_ms(label):  # median over steps of the summed device time of `label` segments
+        per_step = []
+        for marks in phase:
+            t = sum(marks[k - 1][1].elapsed_time(marks[k][1]) for k in range(1, len(marks)) if marks[k][0] == label)
+            per_step.append(t)
+        return statistics.median(per_step)
+    nb = len(role.peers) if role.phase == "prefill" else 1  # batches this rank handles per step
     if eng.pf:
-        pf_ms = med("start", "prefill_end")
-        comp["prefill_ms_per_step"] = pf_ms
+        pf_ms = phase_ms("prefill") / nb
+        comp["prefill_ms_per_batch"] = pf_ms
         comp["prefill_tok_s_per_gpu"] = w.T / (pf_ms / 1e3)
         comp["prefill_tflops"] = w.L * w.prefill_flops_per_layer() / (pf_ms / 1e3) / 1e12
         comp["prefill_frac_of_tensor_peak"] = comp["prefill_tflops"] / peaks["bf16_tflops"]
         t_roof = w.L * max(w.prefill_flops_per_layer() / (peaks["bf16_tflops"] * 1e12),
                            w.prefill_bytes_per_layer() / (peaks["hbm_gbs"] * 1e9))
         comp["prefill_frac_of_attainable_roofline"] = t_roof / (pf_ms / 1e3)
-        mig_ms = med("prefill_end", "migrate_end")
-        comp["migrate_ms_per_step"] = mig_ms
+    if role.phase != "decode" or world > 1:
+        mig_ms = phase_ms("migrate") / nb
+        comp["migrate_ms_per_batch"] = mig_ms
         comp["kv_migrate_GBps"] = w.kv_payload_bytes() / (mig_ms / 1e3) / 1e9
         comp["kv_migrate_page_GBps"] = w.kv_page_bytes() / (mig_ms / 1e3) / 1e9
         comp["kv_migrate_path"] = "LOCAL page copy (one GPU)" if world == 1 else "NCCL p2p over NVLink"
@@ -545,8 +615,8 @@ def run_ds(args):
             comp["kv_migrate_frac_of_nvlink"] = comp["kv_migrate_page_GBps"] / NVLINK_GBS
     dec_kernel = None
     if eng.dc:
-        dec_ms = med("migrate_end", "end")
-        comp["decode_ms_per_step"] = dec_ms
+        dec_ms = phase_ms("decode")
+        comp["decode_ms_per_batch"] = dec_ms
         comp["decode_tok_s_per_gpu"] = w.B * w.out_len / (dec_ms / 1e3)
         ctx_steps = [[c + s for c in w.lens] for s in range(w.out_len)]
         avg_bytes = sum(w.decode_bytes(c) for c in ctx_steps) / w.out_len
@@ -579,8 +649,10 @@ def run_ds(args):
     line = {"metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": _config_line(w, world, replicas), "components": comp, "roofline": roofline,
+            "config": _config_line(w, world, replicas, roles), "components": comp, "roofline": roofline,
             "clocks": clocks, "gpu_launches": eng.launches}
+    if world > 1:
+        comp.update(measure_migration(eng, w, world, torch))
     if not args.no_e2e:
         line["e2e"] = run_e2e(args, eng, w, world, replicas, torch)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -608,6 +680,42 @@ def run_ds(args):
         dist.destroy_process_group()
 
 
+def measure_migration(eng, w, world, torch, reps=3):
+    """N>1: the KV migration alone, all prefill ranks sending to all their decode
+    ranks in lockstep after a barrier (the pipelined step also contains waits for
+    the peer, so its migrate segments understate the link). Per prefill rank:
+    page bytes moved / device time, against NVLink per direction."""
+    ds, role = eng.ds, eng.role
+    if eng.pf:
+        tp = np.full((w.B, w.maxb), -1, np.int32)
+        ds.ds_block_table(eng.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
+        src_ids = eng.page_ids(eng.upload(tp))
+    else:
+        eng.admit()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        if eng.pf:
+            for peer in role.peers:
+                ds.ds_kv_migrate(eng.comm, eng.mrole, peer, eng.P, 0, w.L, src_ids, 0, w.n, eng.staging)
+        else:
+            ds.ds_kv_migrate(eng.comm, eng.mrole, role.peer, eng.D, 0, w.L, eng.dst_ids, 0, w.n, eng.staging)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    if eng.pf:
+        ds.ds_block_table(eng.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
+    else:
+        ds.ds_block_table(eng.pool_d, ds.DS_BT_FREE, w.lens, None, eng.td)
+    nb = len(role.peers) if eng.pf else 1
+    gbps = reps * nb * w.kv_page_bytes() / (ms / 1e3) / 1e9
+    return {"kv_migrate_isolated_GBps": gbps, "kv_migrate_isolated_frac_of_nvlink": gbps / NVLINK_GBS,
+            "kv_migrate_isolated_ms_per_batch": ms / (reps * nb)}
+
+
 def run_e2e(args, eng, w, world, replicas, torch):
     """The same step through the same API, but every layer's prefill inputs and
     every decode step's inputs are copied host(pinned)->device inside the timed
@@ -621,24 +729,45 @@ def run_e2e(args, eng, w, world, replicas, torch):
         host["dec"] = torch.randn((3,) + tuple(eng.dq.shape), dtype=torch.float32).to(bf).pin_memory()
         host["out"] = torch.empty(tuple(eng.dout.shape), dtype=bf).pin_memory()
 
-    def step():
+    def copy_prefill_inputs():
+        nonlocal h2d
+        for layer in range(w.L):  # every layer's inputs cross PCIe (into the rotating resident buffers)
+            i = layer % len(eng.q)
+            eng.q[i].copy_(host["qkv"][0], non_blocking=True)
+            eng.k[i].copy_(host["qkv"][1], non_blocking=True)
+            eng.v[i].copy_(host["qkv"][2], non_blocking=True)
+            h2d += 3 * host["qkv"][0].numel() * 2
+
+    def decode_io(after):
         nonlocal h2d, d2h
-        if eng.pf:  # every layer's inputs cross PCIe (into the rotating resident buffers)
-            for layer in range(w.L):
-                i = layer % len(eng.q)
-                eng.q[i].copy_(host["qkv"][0], non_blocking=True)
-                eng.k[i].copy_(host["qkv"][1], non_blocking=True)
-                eng.v[i].copy_(host["qkv"][2], non_blocking=True)
-                h2d += 3 * host["qkv"][0].numel() * 2
-        if eng.dc:
+        if not after:
             eng.dq.copy_(host["dec"][0], non_blocking=True)
             eng.dk.copy_(host["dec"][1], non_blocking=True)
             eng.dv.copy_(host["dec"][2], non_blocking=True)
             h2d += 3 * eng.dq.numel() * 2
-        eng.step()
-        if eng.dc:
+        else:
             host["out"].copy_(eng.dout, non_blocking=True)
             d2h += eng.dout.numel() * 2
+
+    def step():  # Engine.step with the host <-> device traffic of every batch
+        role = eng.role
+        if role.phase == "both":
+            copy_prefill_inputs()
+            decode_io(False)
+            eng.admit()
+            eng.prefill_and_send(0, None)
+            eng.decode_batch(None)
+            decode_io(True)
+        elif role.phase == "prefill":
+            for peer in role.peers:
+                copy_prefill_inputs()
+                eng.prefill_and_send(peer, None)
+        else:
+            decode_io(False)
+            eng.admit()
+            eng.ds.ds_kv_migrate(eng.comm, eng.mrole, role.peer, eng.D, 0, w.L, eng.dst_ids, 0, w.n, eng.staging)
+            eng.decode_batch(None)
+            decode_io(True)
 
     step()
     torch.cuda.synchronize()
@@ -651,6 +780,11 @@ def run_e2e(args, eng, w, world, replicas, torch):
     e1.record()
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), world) / args.e2e_steps
+    if world > 1:  # whole-job host <-> device bytes
+        import torch.distributed as dist
+        t = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        h2d, d2h = int(t[0].item()), int(t[1].item())
     return {"value": replicas * (w.T + w.B * w.out_len) / (ms / 1e3), "unit": "tok/s",
             "h2d_bytes_per_step": h2d // args.e2e_steps, "d2h_bytes_per_step": d2h // args.e2e_steps,
             "ms_per_step": ms, "steps": args.e2e_steps}

@@ -12,7 +12,15 @@ with. Follows the paper's placement structure:
   * "KV cache transfer occurs exclusively between corresponding layers"
     (P:363): the prefill rank (replica, stage, tp) pairs with the decode rank
     (replica, stage, tp) — same layer range, same head range;
-  * replication: independent (prefill, decode) instance pairs.
+  * replication: independent (prefill, decode) instance pairs (P:120);
+  * unequal phase sizes: "allocation of multiple prefill instances to a single
+    decoding instance" — and, for attention-only work where decode
+    dominates, one prefill instance feeding several decoding instances; each
+    prefill instance dispatches its batches round-robin over the decoding
+    instances it serves (FCFS to the least-loaded decoder, degenerates
+    to round-robin for equal batches). The split is chosen from the workload's
+    roofline cost (`balanced_prefill_instances`), as the paper's placement
+    step chooses it from its latency model.
 Both phases use the same (tp, pp) here (BASELINE configs 3-5; reading R18);
 TP-mismatched resharding is SURVEY §8f NEXT-1.
 """
@@ -26,18 +34,24 @@ class RankRole:
     rank: int
     world: int
     phase: str          # "prefill", "decode", or "both" (N = 1: one GPU plays both)
-    replica: int        # instance pair index
+    replica: int        # instance index within its phase
     stage: int          # PP stage within the instance
     tp_rank: int        # TP rank within the stage
-    peer: int           # the rank this one migrates pages with
+    peer: int           # decode: the prefill rank it receives from; prefill: its first decode peer
     layer_begin: int
     layer_count: int
     head_begin: int
     head_count: int
+    peers: tuple = ()   # prefill: every decode rank it feeds, in dispatch order
 
 
-def assign(rank: int, world: int, layers: int, heads: int, tp: int = 1, pp: int = 1) -> RankRole:
-    """Role of `rank` among `world` ranks for a model with `layers` x `heads`."""
+def assign(rank: int, world: int, layers: int, heads: int, tp: int = 1, pp: int = 1,
+           n_prefill: int | None = None) -> RankRole:
+    """Role of `rank` among `world` ranks for a model with `layers` x `heads`.
+
+    n_prefill = number of prefill INSTANCES (each tp*pp ranks); default world/2
+    ranks' worth (1:1). Instances [0, n_prefill) are prefill, the rest decode;
+    decode instance j receives from prefill instance j % n_prefill."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad rank/world")
     if heads % tp or layers % pp:
@@ -46,35 +60,67 @@ def assign(rank: int, world: int, layers: int, heads: int, tp: int = 1, pp: int 
     if world == 1:
         if per_inst != 1:
             raise ValueError("one GPU hosts a single TP1/PP1 instance pair")
-        return RankRole(0, 1, "both", 0, 0, 0, 0, 0, layers, 0, heads)
-    if world % 2 or (world // 2) % per_inst:
-        raise ValueError(f"world={world} must be 2 x (replicas x tp x pp = {per_inst})")
-    half = world // 2
-    phase = "prefill" if rank < half else "decode"
-    local = rank % half
-    replica, idx = divmod(local, per_inst)
+        return RankRole(0, 1, "both", 0, 0, 0, 0, 0, layers, 0, heads, (0,))
+    if world % per_inst:
+        raise ValueError(f"world={world} must be a multiple of tp x pp = {per_inst}")
+    n_inst = world // per_inst
+    if n_prefill is None:
+        if n_inst % 2:
+            raise ValueError(f"world={world} must be 2 x (instances x tp x pp = {per_inst}) for 1:1 pairs")
+        n_prefill = n_inst // 2
+    if not 1 <= n_prefill < n_inst:
+        raise ValueError(f"need 1 <= prefill instances ({n_prefill}) < instances ({n_inst})")
+    n_decode = n_inst - n_prefill
+    inst, idx = divmod(rank, per_inst)
     stage, tp_rank = divmod(idx, tp)
-    peer = rank + half if phase == "prefill" else rank - half
     lc, hc = layers // pp, heads // tp
-    return RankRole(rank, world, phase, replica, stage, tp_rank, peer, stage * lc, lc, tp_rank * hc, hc)
+    if inst < n_prefill:
+        served = tuple((n_prefill + j) * per_inst + idx for j in range(n_decode) if j % n_prefill == inst)
+        if not served:
+            raise ValueError(f"prefill instance {inst} feeds no decoding instance ({n_prefill}:{n_decode})")
+        return RankRole(rank, world, "prefill", inst, stage, tp_rank, served[0], stage * lc, lc, tp_rank * hc, hc,
+                        served)
+    j = inst - n_prefill
+    peer = (j % n_prefill) * per_inst + idx
+    return RankRole(rank, world, "decode", j, stage, tp_rank, peer, stage * lc, lc, tp_rank * hc, hc, (peer,))
 
 
-def all_roles(world: int, layers: int, heads: int, tp: int = 1, pp: int = 1):
-    return [assign(r, world, layers, heads, tp, pp) for r in range(world)]
+def balanced_prefill_instances(world: int, tp: int, pp: int, t_prefill: float, t_decode: float) -> int:
+    """Prefill instances that balance the two phases for a workload whose one
+    batch costs t_prefill on a prefill instance and t_decode on a decoding one
+    (throughput = min(n_p / t_prefill, n_d / t_decode)); at least one of each."""
+    n_inst = world // (tp * pp)
+    if n_inst < 2:
+        raise ValueError("need at least one prefill and one decoding instance")
+    best, best_tp = 1, -1.0
+    for n_p in range(1, n_inst):
+        thr = min(n_p / t_prefill, (n_inst - n_p) / t_decode)
+        if thr > best_tp + 1e-12:
+            best, best_tp = n_p, thr
+    return best
+
+
+def all_roles(world: int, layers: int, heads: int, tp: int = 1, pp: int = 1, n_prefill: int | None = None):
+    return [assign(r, world, layers, heads, tp, pp, n_prefill) for r in range(world)]
 
 
 def check_pairing(roles) -> None:
-    """Invariants of a placement: symmetric pairs, corresponding layer and head
-    ranges, every (layer, head) of every replica covered exactly once per phase."""
+    """Invariants of a placement: every decode rank receives from exactly one
+    prefill rank that lists it; the two hold corresponding layer and head ranges
+    (P:363); every (layer, head) of every instance is covered exactly once."""
     by_rank = {r.rank: r for r in roles}
     for r in roles:
-        if r.phase == "both":
-            continue
-        p = by_rank[r.peer]
-        assert p.peer == r.rank and p.phase != r.phase
-        assert (p.replica, p.stage, p.tp_rank) == (r.replica, r.stage, r.tp_rank)
-        assert (p.layer_begin, p.layer_count, p.head_begin, p.head_count) == \
-               (r.layer_begin, r.layer_count, r.head_begin, r.head_count)
+        if r.phase == "decode":
+            p = by_rank[r.peer]
+            assert p.phase == "prefill" and r.rank in p.peers
+            assert (p.stage, p.tp_rank) == (r.stage, r.tp_rank)
+            assert (p.layer_begin, p.layer_count, p.head_begin, p.head_count) == \
+                   (r.layer_begin, r.layer_count, r.head_begin, r.head_count)
+        elif r.phase == "prefill":
+            for d in r.peers:
+                assert by_rank[d].phase == "decode" and by_rank[d].peer == r.rank
+    fed = [d for r in roles if r.phase == "prefill" for d in r.peers]
+    assert len(fed) == len(set(fed)) == sum(r.phase == "decode" for r in roles)
     cover = {}
     for r in roles:
         for l in range(r.layer_begin, r.layer_begin + r.layer_count):

@@ -84,7 +84,29 @@ def test_placements_pair_corresponding_layers_and_heads(world, layers, heads, tp
         assert r.peer == 1
 
 
+@pytest.mark.parametrize("world,n_p", [(4, 1), (8, 1), (8, 2), (8, 3), (3, 1)])
+def test_unequal_prefill_decode_split(world, n_p):
+    roles = pairing.all_roles(world, 40, 40, n_prefill=n_p)
+    pairing.check_pairing(roles)
+    pre = [r for r in roles if r.phase == "prefill"]
+    dec = [r for r in roles if r.phase == "decode"]
+    assert len(pre) == n_p and len(dec) == world - n_p
+    loads = sorted(len(r.peers) for r in pre)
+    assert loads[-1] - loads[0] <= 1  # round-robin dispatch balances the decoders per prefill rank
+
+
+def test_balanced_split_follows_stage_costs():
+    # decode 6x costlier than prefill: 1 prefill rank for up to ~7 ranks
+    assert pairing.balanced_prefill_instances(2, 1, 1, 1.0, 6.0) == 1
+    assert pairing.balanced_prefill_instances(8, 1, 1, 1.0, 6.0) == 1
+    assert pairing.balanced_prefill_instances(8, 1, 1, 1.0, 1.0) == 4
+    assert pairing.balanced_prefill_instances(8, 1, 1, 3.0, 1.0) == 6
+    assert pairing.balanced_prefill_instances(8, 2, 2, 1.0, 1.0) == 1
+
+
 def test_bad_placements_rejected():
     for args in ((3, 40, 40, 1, 1), (4, 40, 40, 3, 1), (8, 40, 40, 1, 3), (6, 40, 40, 2, 1)):
         with pytest.raises(ValueError):
             pairing.all_roles(*args)
+    with pytest.raises(ValueError):
+        pairing.all_roles(4, 40, 40, n_prefill=4)  # no decoding instance
