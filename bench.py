@@ -76,6 +76,10 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graphs", action="store_true", help="eager decode launches (no CUDA graphs)")
+    p.add_argument("--transport", default="nccl", choices=["nccl", "pull"],
+                   help="N>1 KV migration: NCCL send/recv (default) or one-sided CUDA-IPC pull by the decoder")
+    p.add_argument("--pg-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="torch.distributed backend for plumbing (gloo lets 2 ranks share one GPU for rehearsal)")
     p.add_argument("--prefill-instances", type=int, default=0,
                    help="N>1: prefill instances (0 = balance the phases with the roofline cost model)")
     p.add_argument("--profile", action="store_true", help="one short pass for ncu (no JSON)")
@@ -202,7 +206,7 @@ def _i32(torch, a):
 class Engine:
     """Device state of one rank: pools, resident inputs, staging, CUDA graphs."""
 
-    def __init__(self, w: Workload, role, comm, seed, torch, ds):
+    def __init__(self, w: Workload, role, comm, seed, torch, ds, transport="nccl"):
         self.w, self.role, self.comm, self.torch, self.ds = w, role, comm, torch, ds
         dev = "cuda"
         bf = torch.bfloat16
@@ -212,7 +216,7 @@ class Engine:
         self.dc = role.phase in ("both", "decode")
         # one batch per pool: the prefill side's pages are reused for batch k+1 only after
         # the (stream-ordered) migration of batch k; the decode side admits k+1 after k ends
-        nb_p = sum(w.pages) + 16
+        nb_p = sum(w.pages) * (2 * len(role.peers) if (transport == "pull" and role.phase == "prefill") else 1) + 16
         nb_d = sum(-(-(l + w.out_len) // 16) for l in w.lens) + 16
         if self.pf:
             self.P = ds.KVCache.empty(w.L, nb_p, w.n, w.d)
@@ -247,8 +251,9 @@ class Engine:
             self.hslot = 0
             self.graphs = None
         nblk = sum(w.pages)
-        self.mrole = {"both": ds.DS_MIGRATE_LOCAL, "prefill": ds.DS_MIGRATE_SEND,
-                      "decode": ds.DS_MIGRATE_RECV}[role.phase]
+        self.transport = "local" if role.phase == "both" else transport
+        self.mrole = {"local": ds.DS_MIGRATE_LOCAL, "pull": ds.DS_MIGRATE_PULL}.get(
+            self.transport, ds.DS_MIGRATE_SEND if role.phase == "prefill" else ds.DS_MIGRATE_RECV)
         cache_for_size = self.P if self.pf else self.D
         sbytes = ds.ds_kv_migrate_staging_bytes(cache_for_size, self.mrole, w.L, nblk, w.n)
         self.staging = torch.empty(sbytes, dtype=torch.uint8, device=dev) if sbytes else None
@@ -322,6 +327,8 @@ class Engine:
     def prefill_and_send(self, peer, marks):
         """a1 + a2/a3 for one batch, then a4-a6 towards decode rank `peer`."""
         ds, w = self.ds, self.w
+        if self.transport == "pull":
+            self.pull_reclaim(peer, keep=1)  # a pool slot for this batch
         tp = np.full((w.B, w.maxb), -1, np.int32)
         ds.ds_block_table(self.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
         tp_d = self.upload(tp)
@@ -332,15 +339,96 @@ class Engine:
         self.launches += w.L
         src_ids = self.page_ids(tp_d)
         self._mark(marks, "prefill")
-        if self.mrole == ds.DS_MIGRATE_LOCAL:
+        if self.transport == "local":
             ds.ds_kv_migrate(None, self.mrole, 0, self.P, 0, w.L, src_ids, 0, w.n, None,
                              dst_cache=self.D, dst_block_ids=self.dst_ids)
             self.launches += 1
-        else:
+        elif self.transport == "nccl":
             ds.ds_kv_migrate(self.comm, self.mrole, peer, self.P, 0, w.L, src_ids, 0, w.n, self.staging)
             self.launches += self.migrate_chunks()
+        else:  # pull: publish the batch; the decoder fetches it when it has memory
+            self.pull_publish(peer, tp)
+            self._mark(marks, "migrate")
+            return
         # the pages are free again once the (stream-ordered) migration has read them
         ds.ds_block_table(self.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
+        self._mark(marks, "migrate")
+
+    # -- one-sided pull (CUDA IPC) ----------------------------------------------------
+    def pull_setup(self, roles, ctl):
+        """Exchange pool / event handles: prefill ranks export their pool and one
+        'ready' event per (decoder, slot); decoders export one 'done' event per slot."""
+        import torch.distributed as dist
+        ds, w, role = self.ds, self.w, self.role
+        self.ctl = ctl
+        info = {"rank": role.rank}
+        if role.phase == "prefill":
+            self.ready = {p: [ds.IpcEvent() for _ in range(2)] for p in role.peers}
+            h, off = ds.ds_ipc_export_mem(self.P.tensor)
+            info.update(pool=(h, off, self.P.num_blocks), ready={p: [e.handle for e in evs] for p, evs in self.ready.items()})
+        else:
+            self.done = [ds.IpcEvent() for _ in range(2)]
+            info.update(done=[e.handle for e in self.done])
+        allinfo = [None] * role.world
+        dist.all_gather_object(allinfo, info, group=ctl)
+        if role.phase == "prefill":
+            self.peer_done = {p: [ds.IpcEvent(hd) for hd in allinfo[p]["done"]] for p in role.peers}
+            self.inflight = {p: [] for p in role.peers}
+            self.sent = {p: 0 for p in role.peers}
+        else:
+            src = allinfo[role.peer]
+            h, off, nb = src["pool"]
+            self.remote = ds.RemoteKVCache(h, off, w.L, nb, w.n, w.d)
+            self.peer_ready = [ds.IpcEvent(hd) for hd in src["ready"][role.rank]]
+            self.recvd = 0
+
+    def pull_publish(self, peer, tp):
+        torch, w = self.torch, self.w
+        k = self.sent[peer]
+        self.ready[peer][k % 2].record()
+        ids = np.concatenate([[k], tp[:, :max(w.pages)].reshape(-1)]).astype(np.int32)
+        torch.distributed.send(torch.from_numpy(ids), peer, group=self.ctl)
+        self.inflight[peer].append((k, tp))
+        self.sent[peer] = k + 1
+
+    def pull_reclaim(self, peer, keep):
+        """free this decoder's batches once it has pulled them (at most `keep` left in flight... 2 slots)"""
+        torch, ds, w = self.torch, self.ds, self.w
+        while len(self.inflight[peer]) > keep:
+            k, tp = self.inflight[peer].pop(0)
+            msg = torch.zeros(1, dtype=torch.int32)
+            torch.distributed.recv(msg, peer, group=self.ctl)
+            assert int(msg[0]) == k, (int(msg[0]), k)
+            self.peer_done[peer][k % 2].wait()  # the decoder's pull kernel has read the pages
+            ds.ds_block_table(self.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
+
+    def pull_drain(self):
+        if self.transport == "pull" and self.role.phase == "prefill":
+            for peer in self.role.peers:
+                self.pull_reclaim(peer, keep=0)
+
+    def receive(self, marks):
+        """decode rank: admit the batch, then migrate it in (NCCL recv, or PULL)"""
+        ds, w, role, torch = self.ds, self.w, self.role, self.torch
+        if self.transport == "pull":
+            ids = torch.zeros(1 + w.B * max(w.pages), dtype=torch.int32)
+            torch.distributed.recv(ids, role.peer, group=self.ctl)
+            k = int(ids[0])
+            assert k == self.recvd, (k, self.recvd)
+            tab = ids[1:].numpy().reshape(w.B, max(w.pages))
+            src = np.concatenate([tab[b, :p] for b, p in enumerate(w.pages)])
+            self.admit()
+            self.peer_ready[k % 2].wait()  # the prefill of this batch has finished
+            ds.ds_kv_migrate(None, ds.DS_MIGRATE_PULL, 0, self.remote, 0, w.L, _i32(torch, src), 0, w.n, None,
+                             dst_cache=self.D, dst_block_ids=self.dst_ids)
+            self.done[k % 2].record()
+            torch.distributed.send(torch.tensor([k], dtype=torch.int32), role.peer, group=self.ctl)
+            self.recvd = k + 1
+            self.launches += 1
+        else:
+            self.admit()
+            ds.ds_kv_migrate(self.comm, self.mrole, role.peer, self.D, 0, w.L, self.dst_ids, 0, w.n, self.staging)
+            self.launches += self.migrate_chunks()
         self._mark(marks, "migrate")
 
     def migrate_chunks(self):
@@ -385,10 +473,7 @@ class Engine:
             for peer in role.peers:
                 self.prefill_and_send(peer, marks)
         else:
-            self.admit()
-            ds.ds_kv_migrate(self.comm, self.mrole, role.peer, self.D, 0, w.L, self.dst_ids, 0, w.n, self.staging)
-            self.launches += self.migrate_chunks()
-            self._mark(marks, "migrate")
+            self.receive(marks)
             self.decode_batch(marks)
 
 
@@ -403,7 +488,10 @@ def dist_setup(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.pg_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -412,7 +500,8 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -550,7 +639,11 @@ def run_ds(args):
         comm = ds.ds_comm_init(pairing.bootstrap_unique_id(ds.ds_comm_get_unique_id, rank, world, dist), world, rank)
     replicas = 1 if world == 1 else sum(1 for r in roles if r.phase == "decode") // (cfg["tp"] * cfg["pp"])
     eng = Engine(w, role, comm, seed=1234 + role.replica * 7919 + role.stage * 131 + role.tp_rank, torch=torch,
-                 ds=ds)
+                 ds=ds, transport=args.transport)
+    if world > 1 and args.transport == "pull":
+        import torch.distributed as dist
+        ctl = dist.group.WORLD if args.pg_backend == "gloo" else dist.new_group(backend="gloo")
+        eng.pull_setup(roles, ctl)
     torch.cuda.synchronize()
     if args.profile:
         eng.step()
@@ -561,8 +654,8 @@ def run_ds(args):
     torch.cuda.synchronize()
     if eng.dc and not args.no_graphs:
         eng.capture_decode_graphs()
-        eng.step()  # one graph-replay warm-up step
-        torch.cuda.synchronize()
+    eng.step()  # one more warm-up step on every rank (graph replay on decoders; keeps the pairs in step)
+    torch.cuda.synchronize()
     barrier(world)
     sampler = ClockSampler(local)
     sampler.start()
@@ -610,7 +703,9 @@ def run_ds(args):
         comp["migrate_ms_per_batch"] = mig_ms
         comp["kv_migrate_GBps"] = w.kv_payload_bytes() / (mig_ms / 1e3) / 1e9
         comp["kv_migrate_page_GBps"] = w.kv_page_bytes() / (mig_ms / 1e3) / 1e9
-        comp["kv_migrate_path"] = "LOCAL page copy (one GPU)" if world == 1 else "NCCL p2p over NVLink"
+        comp["kv_migrate_path"] = ("LOCAL page copy (one GPU)" if world == 1 else
+                                   "NCCL p2p over NVLink" if args.transport == "nccl" else
+                                   "one-sided pull: decoder's kernel reads the IPC-mapped prefill pool")
         if world > 1:
             comp["kv_migrate_frac_of_nvlink"] = comp["kv_migrate_page_GBps"] / NVLINK_GBS
     dec_kernel = None
@@ -651,10 +746,12 @@ def run_ds(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": _config_line(w, world, replicas, roles), "components": comp, "roofline": roofline,
             "clocks": clocks, "gpu_launches": eng.launches}
+    eng.pull_drain()
     if world > 1:
         comp.update(measure_migration(eng, w, world, torch))
     if not args.no_e2e:
         line["e2e"] = run_e2e(args, eng, w, world, replicas, torch)
+        eng.pull_drain()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tok_s, threads, sample = oracle_sample_tok_s(w)
         line["cpu_baseline"] = {"value": tok_s, "unit": "tok/s", "cores": threads, "kind": "oracle",
@@ -681,23 +778,37 @@ def run_ds(args):
 
 
 def measure_migration(eng, w, world, torch, reps=3):
-    """N>1: the KV migration alone, all prefill ranks sending to all their decode
-    ranks in lockstep after a barrier (the pipelined step also contains waits for
-    the peer, so its migrate segments understate the link). Per prefill rank:
-    page bytes moved / device time, against NVLink per direction."""
+    """N>1: the KV migration alone, all pairs in lockstep after a barrier (the
+    pipelined step also contains waits for the peer, so its migrate segments
+    understate the link). NCCL: per prefill rank, page bytes sent / device time.
+    PULL: per decoding rank, page bytes pulled / device time."""
     ds, role = eng.ds, eng.role
+    pull = eng.transport == "pull"
     if eng.pf:
         tp = np.full((w.B, w.maxb), -1, np.int32)
         ds.ds_block_table(eng.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
         src_ids = eng.page_ids(eng.upload(tp))
+        if pull:
+            for peer in role.peers:  # publish the same pages to every decoder it feeds
+                ids = np.concatenate([[-1], tp[:, :max(w.pages)].reshape(-1)]).astype(np.int32)
+                torch.distributed.send(torch.from_numpy(ids), peer, group=eng.ctl)
     else:
         eng.admit()
+        if pull:
+            ids = torch.zeros(1 + w.B * max(w.pages), dtype=torch.int32)
+            torch.distributed.recv(ids, role.peer, group=eng.ctl)
+            tab = ids[1:].numpy().reshape(w.B, max(w.pages))
+            pull_src = _i32(torch, np.concatenate([tab[b, :p] for b, p in enumerate(w.pages)]))
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        if eng.pf:
+        if pull:
+            if not eng.pf:
+                ds.ds_kv_migrate(None, ds.DS_MIGRATE_PULL, 0, eng.remote, 0, w.L, pull_src, 0, w.n, None,
+                                 dst_cache=eng.D, dst_block_ids=eng.dst_ids)
+        elif eng.pf:
             for peer in role.peers:
                 ds.ds_kv_migrate(eng.comm, eng.mrole, peer, eng.P, 0, w.L, src_ids, 0, w.n, eng.staging)
         else:
@@ -710,6 +821,8 @@ def measure_migration(eng, w, world, torch, reps=3):
         ds.ds_block_table(eng.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
     else:
         ds.ds_block_table(eng.pool_d, ds.DS_BT_FREE, w.lens, None, eng.td)
+    if pull and eng.pf:
+        return {}
     nb = len(role.peers) if eng.pf else 1
     gbps = reps * nb * w.kv_page_bytes() / (ms / 1e3) / 1e9
     return {"kv_migrate_isolated_GBps": gbps, "kv_migrate_isolated_frac_of_nvlink": gbps / NVLINK_GBS,
@@ -764,8 +877,7 @@ def run_e2e(args, eng, w, world, replicas, torch):
                 eng.prefill_and_send(peer, None)
         else:
             decode_io(False)
-            eng.admit()
-            eng.ds.ds_kv_migrate(eng.comm, eng.mrole, role.peer, eng.D, 0, w.L, eng.dst_ids, 0, w.n, eng.staging)
+            eng.receive(None)
             eng.decode_batch(None)
             decode_io(True)
 
@@ -782,7 +894,8 @@ def run_e2e(args, eng, w, world, replicas, torch):
     ms = max_over_ranks(e0.elapsed_time(e1), world) / args.e2e_steps
     if world > 1:  # whole-job host <-> device bytes
         import torch.distributed as dist
-        t = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device="cuda")
+        t = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64,
+                         device="cuda" if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t)
         h2d, d2h = int(t[0].item()), int(t[1].item())
     return {"value": replicas * (w.T + w.B * w.out_len) / (ms / 1e3), "unit": "tok/s",

@@ -220,6 +220,11 @@ enum { DS_MIGRATE_SEND = 0, DS_MIGRATE_RECV = 1, DS_MIGRATE_SELF = 2, DS_MIGRATE
  *  role LOCAL (both instances on one device, "asynchronous CudaMemcpy"):
  *       one kernel copies the pages straight from `cache` to `dst_cache`; no
  *       communicator (comm may be NULL), no staging (may be NULL / 0).
+ *  role PULL (decode side, see ds_ipc_*): as LOCAL, but `cache` describes the
+ *       prefill rank's pool mapped into this process; the kernel's loads travel
+ *       over NVLink (or stay local when both processes share the GPU).
+ * For LOCAL / PULL, `dst_layer_begin` may differ from `layer_begin` (pools of
+ * different PP stage extents).
  * Chunking: the (layer, kv, block) page-rows are moved in chunks of about
  * 64 MiB (at least one row of head_count pages) through a 2-slot ring in the
  * staging buffer (2 send + 2 receive slots for SELF); the pack of chunk k+1
@@ -236,8 +241,44 @@ ds_status ds_kv_migrate(ds_comm comm, int32_t role, int32_t peer, const ds_kv_ca
                         int32_t layer_begin, int32_t layer_count, const int32_t *block_ids,
                         int32_t num_blocks, int32_t head_begin, int32_t head_count,
                         const ds_kv_cache *dst_cache, const int32_t *dst_block_ids,
-                        int32_t dst_head_begin, void *staging, size_t staging_bytes,
-                        void *stream);
+                        int32_t dst_head_begin, int32_t dst_layer_begin, void *staging,
+                        size_t staging_bytes, void *stream);
+
+/* ======================================================================
+ * a5, one-sided pull: "decoding instances fetch KV cache
+ * from prefill instances as needed, using the GPU memory of prefill instances
+ * as a queuing buffer", intra-node by asynchronous copies.
+ * The prefill rank exports its pool allocation and an inter-process event; the
+ * decode rank maps the pool (NVLink peer memory, or the same GPU) and calls
+ * ds_kv_migrate(role DS_MIGRATE_PULL) with `cache` = the mapped prefill pool
+ * descriptor: ONE kernel gathers the pages straight into its own pool (no
+ * staging, no NCCL). Ordering across processes: the prefill side records its
+ * event after the prefill; the decode side waits on it (ds_event_wait) before
+ * the pull and records its own event after it, which the prefill side waits on
+ * before reusing those pages. The host-side handshake (who recorded what) is
+ * the caller's (e.g. torch.distributed messages).
+ * Handles are 64 opaque bytes (cudaIpcMemHandle_t / cudaIpcEventHandle_t).
+ * ==================================================================== */
+enum { DS_MIGRATE_PULL = 4 };
+typedef struct {
+  unsigned char bytes[64];
+} ds_ipc_handle;
+/* Export the cudaMalloc allocation that contains `ptr` (e.g. a torch tensor inside
+ * the caching allocator's segment): handle of the allocation + byte offset of ptr.
+ * The importer maps the allocation (ds_ipc_open_mem returns its base) and adds
+ * the offset; the exporting process must keep the memory alive while mapped. */
+ds_status ds_ipc_export_mem(const void *ptr, ds_ipc_handle *handle_h, size_t *offset_h);
+ds_status ds_ipc_open_mem(const ds_ipc_handle *handle_h, void **base_h);
+ds_status ds_ipc_close_mem(void *base);
+
+typedef struct ds_event_s *ds_event;
+/* an inter-process event of the current device (timing disabled) and its handle */
+ds_status ds_event_create_ipc(ds_event *out_h, ds_ipc_handle *handle_h);
+ds_status ds_event_open_ipc(const ds_ipc_handle *handle_h, ds_event *out_h);
+ds_status ds_event_record(ds_event ev, void *stream);
+/* make `stream` wait for the event's most recent record (as seen by this host) */
+ds_status ds_event_wait(ds_event ev, void *stream);
+ds_status ds_event_destroy(ds_event ev);
 
 #ifdef __cplusplus
 }

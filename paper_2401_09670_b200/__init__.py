@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_PKG, "libds.so")
 
 DS_OK, DS_ERR_INVALID_ARG, DS_ERR_UNSUPPORTED, DS_ERR_NO_BLOCKS, DS_ERR_CUDA, DS_ERR_NCCL, DS_ERR_STATE = range(7)
 DS_BT_APPEND, DS_BT_FREE = 0, 1
-DS_MIGRATE_SEND, DS_MIGRATE_RECV, DS_MIGRATE_SELF, DS_MIGRATE_LOCAL = 0, 1, 2, 3
+DS_MIGRATE_SEND, DS_MIGRATE_RECV, DS_MIGRATE_SELF, DS_MIGRATE_LOCAL, DS_MIGRATE_PULL = 0, 1, 2, 3, 4
 BLOCK_SIZE = 16
 
 # every symbol include/ds.h declares (checked by tests/test_abi.py)
@@ -29,7 +29,9 @@ EXPORTED = (
     "ds_last_error", "ds_build_info", "ds_pool_create", "ds_pool_destroy", "ds_pool_num_free",
     "ds_block_table", "ds_prefill_attn", "ds_decode_workspace_bytes", "ds_decode_attn",
     "ds_kv_staging_bytes", "ds_kv_pack", "ds_kv_unpack", "ds_comm_get_unique_id", "ds_comm_init",
-    "ds_comm_destroy", "ds_kv_migrate_staging_bytes", "ds_kv_migrate",
+    "ds_comm_destroy", "ds_kv_migrate_staging_bytes", "ds_kv_migrate", "ds_ipc_export_mem", "ds_ipc_open_mem",
+    "ds_ipc_close_mem", "ds_event_create_ipc", "ds_event_open_ipc", "ds_event_record", "ds_event_wait",
+    "ds_event_destroy",
 )
 
 
@@ -69,8 +71,16 @@ def _load():
         "ds_comm_init": ([P, i32, i32, ctypes.POINTER(P)], ctypes.c_int),
         "ds_comm_destroy": ([P], ctypes.c_int),
         "ds_kv_migrate_staging_bytes": ([cache_p, i32, i32, i32, i32], sz),
-        "ds_kv_migrate": ([P, i32, i32, cache_p, i32, i32, P, i32, i32, i32, cache_p, P, i32, P, sz, P],
+        "ds_kv_migrate": ([P, i32, i32, cache_p, i32, i32, P, i32, i32, i32, cache_p, P, i32, i32, P, sz, P],
                           ctypes.c_int),
+        "ds_ipc_export_mem": ([P, P, ctypes.POINTER(sz)], ctypes.c_int),
+        "ds_ipc_open_mem": ([P, ctypes.POINTER(P)], ctypes.c_int),
+        "ds_ipc_close_mem": ([P], ctypes.c_int),
+        "ds_event_create_ipc": ([ctypes.POINTER(P), P], ctypes.c_int),
+        "ds_event_open_ipc": ([P, ctypes.POINTER(P)], ctypes.c_int),
+        "ds_event_record": ([P, P], ctypes.c_int),
+        "ds_event_wait": ([P, P], ctypes.c_int),
+        "ds_event_destroy": ([P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -308,9 +318,10 @@ def ds_kv_migrate_staging_bytes(cache: KVCache, role: int, layer_count: int, num
     return int(_lib.ds_kv_migrate_staging_bytes(cache.ref(), role, layer_count, num_blocks, head_count))
 
 
-def ds_kv_migrate(comm: Comm, role: int, peer: int, cache: KVCache, layer_begin: int, layer_count: int,
+def ds_kv_migrate(comm: Comm | None, role: int, peer: int, cache, layer_begin: int, layer_count: int,
                   block_ids, head_begin: int, head_count: int, staging, dst_cache: KVCache | None = None,
-                  dst_block_ids=None, dst_head_begin: int = 0, stream=None):
+                  dst_block_ids=None, dst_head_begin: int = 0, dst_layer_begin: int | None = None, stream=None):
+    """`cache` is a KVCache, or (PULL) a RemoteKVCache mapped from another process."""
     torch = _torch()
     _dev(block_ids, torch.int32, "block_ids")
     if dst_block_ids is not None:
@@ -318,5 +329,65 @@ def ds_kv_migrate(comm: Comm, role: int, peer: int, cache: KVCache, layer_begin:
     _check(_lib.ds_kv_migrate(None if comm is None else comm._h, role, peer, cache.ref(), layer_begin, layer_count,
                               block_ids.data_ptr(), block_ids.numel(), head_begin, head_count,
                               None if dst_cache is None else dst_cache.ref(), _ptr(dst_block_ids),
-                              dst_head_begin, _ptr(staging), 0 if staging is None else _nbytes(staging),
-                              _stream(stream)))
+                              dst_head_begin, layer_begin if dst_layer_begin is None else dst_layer_begin,
+                              _ptr(staging), 0 if staging is None else _nbytes(staging), _stream(stream)))
+
+
+# --------------------------------------------------------------------- a5, one-sided pull (CUDA IPC)
+def ds_ipc_export_mem(tensor) -> tuple[bytes, int]:
+    """(64-byte handle of the cudaMalloc allocation holding tensor.data_ptr(),
+    byte offset of the tensor inside it)."""
+    buf = ctypes.create_string_buffer(64)
+    off = ctypes.c_size_t()
+    _check(_lib.ds_ipc_export_mem(tensor.data_ptr(), buf, ctypes.byref(off)))
+    return buf.raw, off.value
+
+
+class RemoteKVCache:
+    """A prefill rank's KV pool mapped into this process (ds_ipc_open_mem);
+    usable as the source `cache` of ds_kv_migrate(DS_MIGRATE_PULL)."""
+
+    def __init__(self, handle: bytes, offset: int, layers: int, num_blocks: int, heads: int, head_dim: int):
+        base = ctypes.c_void_p()
+        buf = ctypes.create_string_buffer(handle, 64)
+        _check(_lib.ds_ipc_open_mem(buf, ctypes.byref(base)))
+        self.base = base.value
+        self.desc = ds_kv_cache(self.base + offset, layers, num_blocks, heads, BLOCK_SIZE, head_dim)
+
+    def ref(self):
+        return ctypes.byref(self.desc)
+
+    def close(self):
+        if getattr(self, "base", None):
+            _lib.ds_ipc_close_mem(self.base)
+            self.base = None
+
+    __del__ = close
+
+
+class IpcEvent:
+    """Inter-process CUDA event: create() here and share .handle, or open(handle)."""
+
+    def __init__(self, handle: bytes | None = None):
+        h = ctypes.c_void_p()
+        if handle is None:
+            buf = ctypes.create_string_buffer(64)
+            _check(_lib.ds_event_create_ipc(ctypes.byref(h), buf))
+            self.handle = buf.raw
+        else:
+            _check(_lib.ds_event_open_ipc(ctypes.create_string_buffer(handle, 64), ctypes.byref(h)))
+            self.handle = handle
+        self._h = h
+
+    def record(self, stream=None):
+        _check(_lib.ds_event_record(self._h, _stream(stream)))
+
+    def wait(self, stream=None):
+        _check(_lib.ds_event_wait(self._h, _stream(stream)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.ds_event_destroy(self._h)
+            self._h = None
+
+    __del__ = close

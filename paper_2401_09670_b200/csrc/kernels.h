@@ -42,7 +42,7 @@ struct KvLocalArgs {
   const uint16_t *src;
   uint16_t *dst;
   const int32_t *src_ids, *dst_ids;  // [num_blocks_sel]
-  int32_t layer_begin, layer_count, num_blocks_sel, head_count, head_dim;
+  int32_t layer_begin, dst_layer_begin, layer_count, num_blocks_sel, head_count, head_dim;
   int32_t src_blocks, src_heads, src_head0, dst_blocks, dst_heads, dst_head0;
 };
 cudaError_t launch_kv_local(const KvLocalArgs &a, cudaStream_t stream);

@@ -64,8 +64,9 @@ __global__ void __launch_bounds__(kThreads) kv_copy_kernel(const KvCopyArgs a) {
   }
 }
 
-// LOCAL migration (both instances on one device): pool row -> pool row directly,
-// no staging buffer and no NCCL ("asynchronous CudaMemcpy" intra-device).
+// LOCAL / PULL migration: pool row -> pool row directly, no staging buffer and
+// no NCCL ("asynchronous CudaMemcpy"). For PULL the source pool is a
+// peer GPU's allocation mapped through CUDA IPC, so the loads cross NVLink.
 __global__ void __launch_bounds__(kThreads) kv_local_kernel(const KvLocalArgs a) {
   const int64_t page_bytes = 16LL * a.head_dim * 2;
   const int64_t row_bytes = page_bytes * a.head_count;
@@ -78,10 +79,10 @@ __global__ void __launch_bounds__(kThreads) kv_local_kernel(const KvLocalArgs a)
     const int64_t r = it / segs_per_row, seg = it % segs_per_row;
     const int64_t i = r % a.num_blocks_sel;
     const int64_t kv = (r / a.num_blocks_sel) & 1;
-    const int64_t layer = a.layer_begin + r / (2LL * a.num_blocks_sel);
-    const char *src = reinterpret_cast<const char *>(a.src) + (2 * layer + kv) * src_kv +
+    const int64_t l = r / (2LL * a.num_blocks_sel);
+    const char *src = reinterpret_cast<const char *>(a.src) + (2 * (a.layer_begin + l) + kv) * src_kv +
                       ((int64_t)a.src_ids[i] * a.src_heads + a.src_head0) * page_bytes;
-    char *dst = reinterpret_cast<char *>(a.dst) + (2 * layer + kv) * dst_kv +
+    char *dst = reinterpret_cast<char *>(a.dst) + (2 * (a.dst_layer_begin + l) + kv) * dst_kv +
                 ((int64_t)a.dst_ids[i] * a.dst_heads + a.dst_head0) * page_bytes;
     const int64_t base = seg * kSegBytes;
     uint4 v[kUnroll];

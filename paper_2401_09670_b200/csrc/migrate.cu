@@ -11,6 +11,7 @@
 // protocol. Pages are gathered (a4) into a chunk ring in the staging buffer on
 // the caller's stream while NCCL moves the previous chunk on a library-owned
 // side stream; the receiver scatters (a6) chunk k while chunk k+1 is in flight.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdio.h>
@@ -79,7 +80,7 @@ extern "C" size_t ds_kv_migrate_staging_bytes(const ds_kv_cache *cache, int32_t 
   if (!cache || layer_count <= 0 || num_blocks <= 0 || head_count <= 0) return 0;
   const int64_t row_bytes = (int64_t)head_count * 16 * cache->head_dim * 2;
   const int64_t rows = (int64_t)layer_count * 2 * num_blocks;
-  if (role == DS_MIGRATE_LOCAL) return 0;
+  if (role == DS_MIGRATE_LOCAL || role == DS_MIGRATE_PULL) return 0;
   const int64_t slots = role == DS_MIGRATE_SELF ? 4 : 2;
   return (size_t)(slots * chunk_rows_for(row_bytes, rows) * row_bytes);
 }
@@ -140,18 +141,19 @@ extern "C" ds_status ds_comm_destroy(ds_comm c) {
 static ds_status migrate_local(const ds_kv_cache *src, int32_t layer_begin, int32_t layer_count,
                                const int32_t *src_ids, int32_t num_blocks, int32_t src_h0,
                                int32_t head_count, const ds_kv_cache *dst, const int32_t *dst_ids,
-                               int32_t dst_h0, void *stream) {
-  const char *W = "ds_kv_migrate(LOCAL)";
+                               int32_t dst_h0, int32_t dst_layer_begin, void *stream) {
+  const char *W = "ds_kv_migrate(LOCAL/PULL)";
   if (!src || !dst) return fail(DS_ERR_INVALID_ARG, "%s: NULL cache", W);
   if (layer_count < 0 || num_blocks < 0 || head_count < 0)
     return fail(DS_ERR_INVALID_ARG, "%s: negative count", W);
   const ds_kv_cache *ends[2] = {src, dst};
   const int32_t h0s[2] = {src_h0, dst_h0};
+  const int32_t l0s[2] = {layer_begin, dst_layer_begin};
   for (int e = 0; e < 2; ++e) {
     const ds_kv_cache *c = ends[e];
     if (!c->base || c->block_size != 16 || (c->head_dim != 64 && c->head_dim != 128))
       return fail(DS_ERR_INVALID_ARG, "%s: bad cache descriptor", W);
-    if (layer_begin < 0 || layer_begin + layer_count > c->num_layers)
+    if (l0s[e] < 0 || l0s[e] + layer_count > c->num_layers)
       return fail(DS_ERR_INVALID_ARG, "%s: layer range outside the pool", W);
     if (h0s[e] < 0 || h0s[e] + head_count > c->num_heads)
       return fail(DS_ERR_INVALID_ARG, "%s: head slice outside n_loc", W);
@@ -165,6 +167,7 @@ static ds_status migrate_local(const ds_kv_cache *src, int32_t layer_begin, int3
   a.src_ids = src_ids;
   a.dst_ids = dst_ids;
   a.layer_begin = layer_begin;
+  a.dst_layer_begin = dst_layer_begin;
   a.layer_count = layer_count;
   a.num_blocks_sel = num_blocks;
   a.head_count = head_count;
@@ -185,12 +188,12 @@ extern "C" ds_status ds_kv_migrate(ds_comm comm, int32_t role, int32_t peer,
                                    int32_t layer_count, const int32_t *block_ids,
                                    int32_t num_blocks, int32_t head_begin, int32_t head_count,
                                    const ds_kv_cache *dst_cache, const int32_t *dst_block_ids,
-                                   int32_t dst_head_begin, void *staging, size_t staging_bytes,
-                                   void *stream) {
+                                   int32_t dst_head_begin, int32_t dst_layer_begin, void *staging,
+                                   size_t staging_bytes, void *stream) {
   const char *W = "ds_kv_migrate";
-  if (role == DS_MIGRATE_LOCAL) return migrate_local(cache, layer_begin, layer_count, block_ids, num_blocks,
-                                                     head_begin, head_count, dst_cache, dst_block_ids,
-                                                     dst_head_begin, stream);
+  if (role == DS_MIGRATE_LOCAL || role == DS_MIGRATE_PULL)
+    return migrate_local(cache, layer_begin, layer_count, block_ids, num_blocks, head_begin, head_count, dst_cache,
+                         dst_block_ids, dst_head_begin, dst_layer_begin, stream);
   if (!comm || !comm->comm) return fail(DS_ERR_STATE, "%s: invalid communicator", W);
   if (role != DS_MIGRATE_SEND && role != DS_MIGRATE_RECV && role != DS_MIGRATE_SELF)
     return fail(DS_ERR_INVALID_ARG, "%s: bad role", W);
@@ -274,5 +277,106 @@ extern "C" ds_status ds_kv_migrate(ds_comm comm, int32_t role, int32_t peer,
   // the caller's stream is ordered after every transfer of this call
   DS_CUDA(cudaEventRecord(comm->ev_start, B), W);
   DS_CUDA(cudaStreamWaitEvent(A, comm->ev_start, 0), W);
+  return DS_OK;
+}
+
+// ---------------------------------------------------------------- CUDA IPC (PULL)
+struct ds_event_s {
+  cudaEvent_t ev = nullptr;
+};
+
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr *, size_t *, CUdeviceptr);
+
+extern "C" ds_status ds_ipc_export_mem(const void *ptr, ds_ipc_handle *handle_h, size_t *offset_h) {
+  const char *W = "ds_ipc_export_mem";
+  if (!ptr || !handle_h || !offset_h) return fail(DS_ERR_INVALID_ARG, "%s: NULL argument", W);
+  static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(ds_ipc_handle), "IPC handle size");
+  // the handle names the whole cudaMalloc allocation; report where `ptr` sits in it
+  static PFN_getAddressRange range_fn = nullptr;
+  if (!range_fn) {
+    void *fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(DS_ERR_CUDA, "%s: cuMemGetAddressRange unavailable", W);
+    range_fn = reinterpret_cast<PFN_getAddressRange>(fp);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return fail(DS_ERR_CUDA, "%s: pointer is not device memory", W);
+  cudaIpcMemHandle_t h;
+  DS_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void *>(base)), W);
+  memcpy(handle_h->bytes, &h, sizeof h);
+  *offset_h = (size_t)(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  return DS_OK;
+}
+
+extern "C" ds_status ds_ipc_open_mem(const ds_ipc_handle *handle_h, void **base_h) {
+  const char *W = "ds_ipc_open_mem";
+  if (!handle_h || !base_h) return fail(DS_ERR_INVALID_ARG, "%s: NULL argument", W);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle_h->bytes, sizeof h);
+  DS_CUDA(cudaIpcOpenMemHandle(base_h, h, cudaIpcMemLazyEnablePeerAccess), W);
+  return DS_OK;
+}
+
+extern "C" ds_status ds_ipc_close_mem(void *base) {
+  if (!base) return fail(DS_ERR_INVALID_ARG, "ds_ipc_close_mem: NULL");
+  DS_CUDA(cudaIpcCloseMemHandle(base), "ds_ipc_close_mem");
+  return DS_OK;
+}
+
+extern "C" ds_status ds_event_create_ipc(ds_event *out_h, ds_ipc_handle *handle_h) {
+  const char *W = "ds_event_create_ipc";
+  if (!out_h || !handle_h) return fail(DS_ERR_INVALID_ARG, "%s: NULL argument", W);
+  static_assert(sizeof(cudaIpcEventHandle_t) == sizeof(ds_ipc_handle), "IPC event handle size");
+  ds_event e = new (std::nothrow) ds_event_s();
+  if (!e) return fail(DS_ERR_INVALID_ARG, "%s: out of host memory", W);
+  cudaError_t err = cudaEventCreateWithFlags(&e->ev, cudaEventInterprocess | cudaEventDisableTiming);
+  cudaIpcEventHandle_t h;
+  if (err == cudaSuccess) err = cudaIpcGetEventHandle(&h, e->ev);
+  if (err != cudaSuccess) {
+    if (e->ev) cudaEventDestroy(e->ev);
+    delete e;
+    return fail(DS_ERR_CUDA, "%s: %s", W, cudaGetErrorString(err));
+  }
+  memcpy(handle_h->bytes, &h, sizeof h);
+  *out_h = e;
+  return DS_OK;
+}
+
+extern "C" ds_status ds_event_open_ipc(const ds_ipc_handle *handle_h, ds_event *out_h) {
+  const char *W = "ds_event_open_ipc";
+  if (!out_h || !handle_h) return fail(DS_ERR_INVALID_ARG, "%s: NULL argument", W);
+  ds_event e = new (std::nothrow) ds_event_s();
+  if (!e) return fail(DS_ERR_INVALID_ARG, "%s: out of host memory", W);
+  cudaIpcEventHandle_t h;
+  memcpy(&h, handle_h->bytes, sizeof h);
+  cudaError_t err = cudaIpcOpenEventHandle(&e->ev, h);
+  if (err != cudaSuccess) {
+    delete e;
+    return fail(DS_ERR_CUDA, "%s: %s", W, cudaGetErrorString(err));
+  }
+  *out_h = e;
+  return DS_OK;
+}
+
+extern "C" ds_status ds_event_record(ds_event e, void *stream) {
+  if (!e || !e->ev) return fail(DS_ERR_STATE, "ds_event_record: invalid event");
+  DS_CUDA(cudaEventRecord(e->ev, static_cast<cudaStream_t>(stream)), "ds_event_record");
+  return DS_OK;
+}
+
+extern "C" ds_status ds_event_wait(ds_event e, void *stream) {
+  if (!e || !e->ev) return fail(DS_ERR_STATE, "ds_event_wait: invalid event");
+  DS_CUDA(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), e->ev, 0), "ds_event_wait");
+  return DS_OK;
+}
+
+extern "C" ds_status ds_event_destroy(ds_event e) {
+  if (!e) return fail(DS_ERR_STATE, "ds_event_destroy: NULL");
+  if (e->ev) cudaEventDestroy(e->ev);
+  delete e;
   return DS_OK;
 }
