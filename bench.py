@@ -632,8 +632,8 @@ def run_ds(args):
     roles = roles_for(cfg, world, args)
     role = roles[rank]
     w = Workload(cfg, args, role)
-    if world == 1:
-        comm = None  # both instances on one GPU: LOCAL page copy, no communicator
+    if world == 1 or args.transport == "pull":
+        comm = None  # LOCAL page copy (one GPU) or CUDA-IPC pull: no NCCL communicator
     else:
         import torch.distributed as dist
         comm = ds.ds_comm_init(pairing.bootstrap_unique_id(ds.ds_comm_get_unique_id, rank, world, dist), world, rank)
