@@ -369,6 +369,7 @@ class Engine:
         else:
             self.done = [ds.IpcEvent() for _ in range(2)]
             info.update(done=[e.handle for e in self.done])
+        self.pending = []  # outstanding non-blocking control messages (work, tensor)
         allinfo = [None] * role.world
         dist.all_gather_object(allinfo, info, group=ctl)
         if role.phase == "prefill":
@@ -386,8 +387,10 @@ class Engine:
         torch, w = self.torch, self.w
         k = self.sent[peer]
         self.ready[peer][k % 2].record()
-        ids = np.concatenate([[k], tp[:, :max(w.pages)].reshape(-1)]).astype(np.int32)
-        torch.distributed.send(torch.from_numpy(ids), peer, group=self.ctl)
+        ids = torch.from_numpy(np.concatenate([[k], tp[:, :max(w.pages)].reshape(-1)]).astype(np.int32))
+        # non-blocking: a blocking send here could wait on a decoder that is itself
+        # blocked handing back its 'done' for an earlier batch
+        self.pending.append((torch.distributed.isend(ids, peer, group=self.ctl), ids))
         self.inflight[peer].append((k, tp))
         self.sent[peer] = k + 1
 
@@ -403,9 +406,14 @@ class Engine:
             ds.ds_block_table(self.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
 
     def pull_drain(self):
-        if self.transport == "pull" and self.role.phase == "prefill":
+        if self.transport != "pull":
+            return
+        if self.role.phase == "prefill":
             for peer in self.role.peers:
                 self.pull_reclaim(peer, keep=0)
+        for work, _ in self.pending:
+            work.wait()
+        self.pending = []
 
     def receive(self, marks):
         """decode rank: admit the batch, then migrate it in (NCCL recv, or PULL)"""
@@ -422,7 +430,8 @@ class Engine:
             ds.ds_kv_migrate(None, ds.DS_MIGRATE_PULL, 0, self.remote, 0, w.L, _i32(torch, src), 0, w.n, None,
                              dst_cache=self.D, dst_block_ids=self.dst_ids)
             self.done[k % 2].record()
-            torch.distributed.send(torch.tensor([k], dtype=torch.int32), role.peer, group=self.ctl)
+            msg = torch.tensor([k], dtype=torch.int32)
+            self.pending.append((torch.distributed.isend(msg, role.peer, group=self.ctl), msg))
             self.recvd = k + 1
             self.launches += 1
         else:
@@ -790,8 +799,8 @@ def measure_migration(eng, w, world, torch, reps=3):
         src_ids = eng.page_ids(eng.upload(tp))
         if pull:
             for peer in role.peers:  # publish the same pages to every decoder it feeds
-                ids = np.concatenate([[-1], tp[:, :max(w.pages)].reshape(-1)]).astype(np.int32)
-                torch.distributed.send(torch.from_numpy(ids), peer, group=eng.ctl)
+                ids = torch.from_numpy(np.concatenate([[-1], tp[:, :max(w.pages)].reshape(-1)]).astype(np.int32))
+                eng.pending.append((torch.distributed.isend(ids, peer, group=eng.ctl), ids))
     else:
         eng.admit()
         if pull:
@@ -821,6 +830,7 @@ def measure_migration(eng, w, world, torch, reps=3):
         ds.ds_block_table(eng.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
     else:
         ds.ds_block_table(eng.pool_d, ds.DS_BT_FREE, w.lens, None, eng.td)
+    eng.pull_drain()
     if pull and eng.pf:
         return {}
     nb = len(role.peers) if eng.pf else 1
