@@ -740,7 +740,7 @@ def run_ds(args):
                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
                     "algorithmic_bytes_per_launch": dec_kernel[0]}
     elif eng.pf:
-        t_layer = comp["prefill_ms_per_step"] / w.L / 1e3
+        t_layer = comp["prefill_ms_per_batch"] / w.L / 1e3
         fl, by = w.prefill_flops_per_layer(), w.prefill_bytes_per_layer()
         if fl / by >= peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9):
             roofline = {"kernel": "ds_prefill_attn (prefill_kernel)", "bound": "tensor",
