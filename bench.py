@@ -707,8 +707,8 @@ def run_ds(args):
         t_roof = w.L * max(w.prefill_flops_per_layer() / (peaks["bf16_tflops"] * 1e12),
                            w.prefill_bytes_per_layer() / (peaks["hbm_gbs"] * 1e9))
         comp["prefill_frac_of_attainable_roofline"] = t_roof / (pf_ms / 1e3)
-    if role.phase != "decode" or world > 1:
-        mig_ms = phase_ms("migrate") / nb
+    if (role.phase != "decode" or world > 1) and not (args.transport == "pull" and role.phase == "prefill"):
+        mig_ms = phase_ms("migrate") / nb  # (a pull prefill rank only publishes; its decoders move the bytes)
         comp["migrate_ms_per_batch"] = mig_ms
         comp["kv_migrate_GBps"] = w.kv_payload_bytes() / (mig_ms / 1e3) / 1e9
         comp["kv_migrate_page_GBps"] = w.kv_page_bytes() / (mig_ms / 1e3) / 1e9
