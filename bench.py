@@ -264,6 +264,7 @@ class Engine:
         self.h_ev = [None] * self.ring
         self.slot = 0
         self.launches = 0
+        self.layer_hook = None  # e2e: per-layer input copies overlapped with the prefill
         idx = np.concatenate([np.arange(b * w.maxb, b * w.maxb + p) for b, p in enumerate(w.pages)])
         self._idx = _i32(torch, idx).long()
 
@@ -334,8 +335,12 @@ class Engine:
         tp_d = self.upload(tp)
         for layer in range(w.L):
             i = layer % len(self.q)
+            if self.layer_hook:
+                self.layer_hook("before", layer)
             ds.ds_prefill_attn(self.q[i], self.k[i], self.v[i], self.out, self.cu, w.max_len, self.P, layer, tp_d,
                                w.scale)
+            if self.layer_hook:
+                self.layer_hook("after", layer)
         self.launches += w.L
         src_ids = self.page_ids(tp_d)
         self._mark(marks, "prefill")
@@ -852,34 +857,68 @@ def run_e2e(args, eng, w, world, replicas, torch):
         host["dec"] = torch.randn((3,) + tuple(eng.dq.shape), dtype=torch.float32).to(bf).pin_memory()
         host["out"] = torch.empty(tuple(eng.dout.shape), dtype=bf).pin_memory()
 
-    def copy_prefill_inputs():
+    # host->device copies ride a separate stream so PCIe overlaps the kernels:
+    # layer l's inputs land in rotating buffer l % n_in; the copy of layer l + n_in
+    # waits until the prefill of layer l has consumed that buffer.
+    main, cs = torch.cuda.current_stream(), torch.cuda.Stream()
+    n_in = len(eng.q) if eng.pf else 0
+    copied = [torch.cuda.Event() for _ in range(w.L)]
+    freed = [torch.cuda.Event() for _ in range(w.L)]
+
+    def copy_layer(layer):
         nonlocal h2d
-        for layer in range(w.L):  # every layer's inputs cross PCIe (into the rotating resident buffers)
-            i = layer % len(eng.q)
+        i = layer % n_in
+        with torch.cuda.stream(cs):
+            if layer >= n_in:
+                cs.wait_event(freed[layer - n_in])
             eng.q[i].copy_(host["qkv"][0], non_blocking=True)
             eng.k[i].copy_(host["qkv"][1], non_blocking=True)
             eng.v[i].copy_(host["qkv"][2], non_blocking=True)
-            h2d += 3 * host["qkv"][0].numel() * 2
+            copied[layer].record(cs)
+        h2d += 3 * host["qkv"][0].numel() * 2
+
+    def hook(when, layer):
+        if when == "before":
+            main.wait_event(copied[layer])
+        else:
+            freed[layer].record(main)
+            if layer + n_in < w.L:
+                copy_layer(layer + n_in)
+
+    def copy_prefill_inputs():
+        cs.wait_stream(main)  # buffers of the previous batch are consumed in stream order
+        for layer in range(min(n_in, w.L)):
+            copy_layer(layer)
+
+    dec_ready = torch.cuda.Event()
 
     def decode_io(after):
         nonlocal h2d, d2h
         if not after:
-            eng.dq.copy_(host["dec"][0], non_blocking=True)
-            eng.dk.copy_(host["dec"][1], non_blocking=True)
-            eng.dv.copy_(host["dec"][2], non_blocking=True)
+            with torch.cuda.stream(cs):
+                cs.wait_stream(main)
+                eng.dq.copy_(host["dec"][0], non_blocking=True)
+                eng.dk.copy_(host["dec"][1], non_blocking=True)
+                eng.dv.copy_(host["dec"][2], non_blocking=True)
+                dec_ready.record(cs)
             h2d += 3 * eng.dq.numel() * 2
         else:
             host["out"].copy_(eng.dout, non_blocking=True)
             d2h += eng.dout.numel() * 2
 
+    def decode_after_inputs():
+        main.wait_event(dec_ready)
+        eng.decode_batch(None)
+
     def step():  # Engine.step with the host <-> device traffic of every batch
         role = eng.role
+        eng.layer_hook = hook if eng.pf else None
         if role.phase == "both":
-            copy_prefill_inputs()
             decode_io(False)
+            copy_prefill_inputs()
             eng.admit()
             eng.prefill_and_send(0, None)
-            eng.decode_batch(None)
+            decode_after_inputs()
             decode_io(True)
         elif role.phase == "prefill":
             for peer in role.peers:
@@ -888,8 +927,9 @@ def run_e2e(args, eng, w, world, replicas, torch):
         else:
             decode_io(False)
             eng.receive(None)
-            eng.decode_batch(None)
+            decode_after_inputs()
             decode_io(True)
+        eng.layer_hook = None
 
     step()
     torch.cuda.synchronize()
@@ -899,6 +939,7 @@ def run_e2e(args, eng, w, world, replicas, torch):
     e0.record()
     for _ in range(args.e2e_steps):
         step()
+    main.wait_stream(cs)
     e1.record()
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), world) / args.e2e_steps
