@@ -140,6 +140,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
       bulk_commit_group();
+      // observe the last stage releases too (every mbarrier phase is waited on;
+      // also guarantees the final MMAs have drained before the CTA retires)
+      for (int t = max(0, ntiles - 2); t < ntiles; ++t) {
+        mbar_wait(&bars[B_KE + (t & 1)], (t >> 1) & 1);
+        mbar_wait(&bars[B_VE + (t & 1)], (t >> 1) & 1);
+      }
       bulk_wait_group_read0();
     }
     __syncwarp();
