@@ -183,6 +183,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         umma_commit(&bars[B_KE + st]);
         if (j >= 1) issue_pv(j - 1);
       }
+      // observe O's second-to-last completion before the last commit (the softmax
+      // only waits on O when it rescales; every phase is waited on by someone)
+      if (ntiles >= 2) mbar_wait(&bars[B_O], (ntiles - 2) & 1);
       issue_pv(ntiles - 1);
     }
     __syncwarp();
