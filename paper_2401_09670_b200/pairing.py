@@ -21,8 +21,12 @@ with. Follows the paper's placement structure:
     to round-robin for equal batches). The split is chosen from the workload's
     roofline cost (`balanced_prefill_instances`), as the paper's placement
     step chooses it from its latency model.
-Both phases use the same (tp, pp) here (BASELINE configs 3-5; reading R18);
-TP-mismatched resharding is SURVEY §8f NEXT-1.
+`assign` uses the same (tp, pp) in both phases (BASELINE configs 3-5; reading
+R18). `reshard_plan` covers the placements the paper actually chose, where the
+phases differ (Table tab:parallel_config: 13B P-TP2 -> D-TP1; 66B
+P-TP4 -> D-TP2 PP2; 175B P-TP3 PP3 -> D-TP4 PP3): each decode
+rank receives the intersection of its (layer, head) rectangle with every prefill
+rank's rectangle.
 """
 from __future__ import annotations
 
@@ -138,3 +142,67 @@ def bootstrap_unique_id(get_id, rank: int, world: int, dist=None) -> bytes:
     obj = [get_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     return obj[0]
+
+
+@dataclasses.dataclass(frozen=True)
+class ReshardSlice:
+    """Pages of `layer_count` layers x `head_count` heads moving from prefill rank
+    `src` to decode rank `dst`; begins are LOCAL indices in each rank's pool."""
+    src: int
+    dst: int
+    src_layer_begin: int
+    dst_layer_begin: int
+    layer_count: int
+    src_head_begin: int
+    dst_head_begin: int
+    head_count: int
+    global_layer_begin: int
+    global_head_begin: int
+
+
+def reshard_plan(layers: int, heads: int, prefill=(1, 1), decode=(1, 1)):
+    """Migration plan from ONE prefill instance (tp_p x pp_p ranks 0..) to ONE
+    decoding instance (tp_d x pp_d ranks following it), rank = stage * tp + tp_rank
+    inside each instance; KV moves only between corresponding layers and
+    TP ranks hold contiguous head ranges (R11). Returns the slices sorted by
+    (dst, src)."""
+    (tp_p, pp_p), (tp_d, pp_d) = prefill, decode
+    for tp, pp in (prefill, decode):
+        if heads % tp or layers % pp:
+            raise ValueError(f"tp={tp}/pp={pp} must divide heads={heads}/layers={layers}")
+    lp, hp, ld, hd = layers // pp_p, heads // tp_p, layers // pp_d, heads // tp_d
+    n_src = tp_p * pp_p
+    out = []
+    for d in range(tp_d * pp_d):
+        sd, td = divmod(d, tp_d)
+        for s in range(n_src):
+            sp, tpp = divmod(s, tp_p)
+            l0, l1 = max(sd * ld, sp * lp), min((sd + 1) * ld, (sp + 1) * lp)
+            h0, h1 = max(td * hd, tpp * hp), min((td + 1) * hd, (tpp + 1) * hp)
+            if l0 < l1 and h0 < h1:
+                out.append(ReshardSlice(s, n_src + d, l0 - sp * lp, l0 - sd * ld, l1 - l0, h0 - tpp * hp,
+                                        h0 - td * hd, h1 - h0, l0, h0))
+    return out
+
+
+def check_reshard(plan, layers: int, heads: int, prefill=(1, 1), decode=(1, 1)) -> None:
+    """Every (layer, head) of every decode rank arrives exactly once, from the
+    prefill rank that computed it, at the same global (layer, head)."""
+    (tp_p, pp_p), (tp_d, pp_d) = prefill, decode
+    lp, hp, ld, hd = layers // pp_p, heads // tp_p, layers // pp_d, heads // tp_d
+    n_src = tp_p * pp_p
+    got = {}
+    for sl in plan:
+        sp, tpp = divmod(sl.src, tp_p)
+        sd, td = divmod(sl.dst - n_src, tp_d)
+        for dl in range(sl.layer_count):
+            for dh in range(sl.head_count):
+                g_src = (sp * lp + sl.src_layer_begin + dl, tpp * hp + sl.src_head_begin + dh)
+                g_dst = (sd * ld + sl.dst_layer_begin + dl, td * hd + sl.dst_head_begin + dh)
+                assert g_src == g_dst, (sl, g_src, g_dst)
+                assert 0 <= sl.src_layer_begin + dl < lp and 0 <= sl.src_head_begin + dh < hp
+                assert 0 <= sl.dst_layer_begin + dl < ld and 0 <= sl.dst_head_begin + dh < hd
+                key = (sl.dst, g_dst)
+                assert key not in got, f"{key} delivered twice"
+                got[key] = sl.src
+    assert len(got) == tp_d * pp_d * ld * hd  # == layers * heads: everything arrives

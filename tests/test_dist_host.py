@@ -110,3 +110,22 @@ def test_bad_placements_rejected():
             pairing.all_roles(*args)
     with pytest.raises(ValueError):
         pairing.all_roles(4, 40, 40, n_prefill=4)  # no decoding instance
+
+
+@pytest.mark.parametrize("layers,heads,prefill,decode", [
+    (40, 40, (2, 1), (1, 1)),    # OPT-13B: P TP2 -> D TP1
+    (64, 72, (4, 1), (2, 2)),    # OPT-66B: P TP4 -> D TP2 PP2
+    (96, 96, (3, 3), (4, 3)),    # OPT-175B: P TP3 PP3 -> D TP4 PP3
+    (8, 12, (3, 2), (2, 4)),     # odd mix: both TP and PP differ
+    (4, 4, (1, 1), (1, 1)),
+])
+def test_reshard_plan_covers_everything_once(layers, heads, prefill, decode):
+    plan = pairing.reshard_plan(layers, heads, prefill, decode)
+    pairing.check_reshard(plan, layers, heads, prefill, decode)
+
+
+def test_reshard_plan_175b_overlaps():
+    # TP3 -> TP4 over 96 heads: decode rank (tp 1) gets heads 24..31 from P tp0 and 32..47 from P tp1
+    plan = [p for p in pairing.reshard_plan(96, 96, (3, 3), (4, 3)) if p.dst == 9 + 1]
+    assert [(p.src, p.global_head_begin, p.head_count) for p in plan] == [(0, 24, 8), (1, 32, 16)]
+    assert all(p.layer_count == 32 and p.src_layer_begin == 0 and p.dst_layer_begin == 0 for p in plan)

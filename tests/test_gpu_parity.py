@@ -359,3 +359,75 @@ def test_invalid_args_raise_before_launch():
     with pytest.raises(ds.DSError) as ei:
         ds.ds_prefill_attn(q, q, q, q, i32([0, 3]), 3, c, 1, i32([[0]]), 0.125)
     assert ei.value.status == ds.DS_ERR_INVALID_ARG
+
+
+@pytest.mark.parametrize("prefill,decode", [((4, 1), (2, 2)), ((3, 1), (4, 1)), ((2, 1), (1, 1))])
+def test_reshard_tp_pp_mismatch_bit_exact(oracle_mod, prefill, decode):
+    """the placements the paper chose have different TP/PP per
+    phase. Every decode rank gathers the intersection of its (layer,
+    head) rectangle from every prefill rank (pairing.reshard_plan), here through the
+    same page-gather kernel PULL uses (LOCAL: all 'ranks' are pools on one GPU)."""
+    from paper_2401_09670_b200 import pairing
+    L, n, d = 4, 12, 64
+    lens = [40, 17, 33]
+    tp_p, pp_p = prefill
+    tp_d, pp_d = decode
+    plan = pairing.reshard_plan(L, n, prefill, decode)
+    pairing.check_reshard(plan, L, n, prefill, decode)
+    layers_in = [syn.prefill_batch(100 + l, lens, n, d) for l in range(L)]
+    # oracle: the whole model's pages in one pool
+    opool = oracle_mod.Pool(L, 16, n, d)
+    t_o = np.full((3, 4), -1, np.int32)
+    opool.append([0] * 3, lens, t_o)
+    for l in range(L):
+        opool.write_prefill(l, layers_in[l].k, layers_in[l].v, layers_in[l].cu_seqlens, t_o)
+    lp, hp, ld, hd = L // pp_p, n // tp_p, L // pp_d, n // tp_d
+    # prefill ranks: each computes its own layers and heads into its own (fragmented) pool
+    src = {}
+    for s in range(tp_p * pp_p):
+        sp, tpp = divmod(s, tp_p)
+        cache = ds.KVCache.empty(lp, 24, hp, d)
+        pool = ds.Pool(24)
+        ds.ds_block_table(pool, ds.DS_BT_APPEND, [0], [16 * (s + 1)], np.full((1, 8), -1, np.int32))
+        tab = np.full((3, 4), -1, np.int32)
+        ds.ds_block_table(pool, ds.DS_BT_APPEND, [0] * 3, lens, tab)
+        out = torch.empty((sum(lens), hp, d), dtype=torch.bfloat16, device="cuda")
+        for ll in range(lp):
+            b = layers_in[sp * lp + ll]
+            sl = slice(tpp * hp, (tpp + 1) * hp)
+            ds.ds_prefill_attn(to_dev(np.ascontiguousarray(b.q[:, sl])), to_dev(np.ascontiguousarray(b.k[:, sl])),
+                               to_dev(np.ascontiguousarray(b.v[:, sl])), out, i32(b.cu_seqlens), max(lens), cache, ll,
+                               i32(tab), 0.125)
+        ids = np.concatenate([tab[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+        src[s] = (cache, i32(ids), pool)
+    # decode ranks: admit, then gather every slice of the plan
+    n_src = tp_p * pp_p
+    dst = {}
+    for dr in range(tp_d * pp_d):
+        cache = ds.KVCache.empty(ld, 20, hd, d)
+        cache.tensor.zero_()
+        pool = ds.Pool(20)
+        ds.ds_block_table(pool, ds.DS_BT_APPEND, [0], [16 * (2 + dr)], np.full((1, 8), -1, np.int32))
+        tab = np.full((3, 4), -1, np.int32)
+        ds.ds_block_table(pool, ds.DS_BT_APPEND, [0] * 3, lens, tab)
+        ids = np.concatenate([tab[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+        dst[n_src + dr] = (cache, i32(ids), tab, pool)
+    for p in plan:
+        scache, sids, _ = src[p.src]
+        dcache, dids, _, _ = dst[p.dst]
+        ds.ds_kv_migrate(None, ds.DS_MIGRATE_LOCAL, 0, scache, p.src_layer_begin, p.layer_count, sids,
+                         p.src_head_begin, p.head_count, None, dst_cache=dcache, dst_block_ids=dids,
+                         dst_head_begin=p.dst_head_begin, dst_layer_begin=p.dst_layer_begin)
+    torch.cuda.synchronize()
+    for dr in range(tp_d * pp_d):
+        sd, td = divmod(dr, tp_d)
+        dcache, _, tab, _ = dst[n_src + dr]
+        bits = to_bits(dcache.tensor)
+        for ll in range(ld):
+            for hh in range(hd):
+                gl, gh = sd * ld + ll, td * hd + hh
+                for r, l in enumerate(lens):
+                    for t in range(l):
+                        for kv in (0, 1):
+                            ref = opool.page(gl, kv, t_o[r, t // BS], gh)[t % BS]
+                            assert np.array_equal(bits[ll, kv, tab[r, t // BS], hh, t % BS], ref), (dr, ll, hh, r, t)
