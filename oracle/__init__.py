@@ -57,6 +57,7 @@ def lib():
         _lib.oracle_decode.argtypes = [P, i32, P, P, P, P, i32, P, i32, f64, P, i32]
         _lib.oracle_migrate.argtypes = [P, P, i32, i32, P, P, i32, i32, i32, i32]
         _lib.oracle_migrate.restype = i64
+        _lib.oracle_chunked_prefill.argtypes = [P, i32, P, P, P, P, P, i32, P, i32, f64, P, i32]
         _lib.oracle_kv_bytes.argtypes = [i32, i64, i32, i32, i32]
         _lib.oracle_kv_bytes.restype = i64
     return _lib
@@ -163,6 +164,20 @@ class Pool:
         if rc != OK:
             raise ValueError(f"oracle_decode rc={rc}")
         return out
+
+
+def chunked_prefill(pool: "Pool", layer: int, q, k, v, cu_seqlens, prefix_lens, table: np.ndarray, scale: float,
+                    nthreads: int | None = None) -> np.ndarray:
+    """NEXT-3: append a chunk per sequence after its cached prefix and attend
+    (rows of the chunk, fp64 [T][n][d])."""
+    q, k, v, cu, pl = _u16(q), _u16(k), _u16(v), _i32(cu_seqlens), _i32(prefix_lens)
+    T, n, d = q.shape
+    out = np.zeros((T, n, d), dtype=np.float64)
+    rc = lib().oracle_chunked_prefill(pool._h, layer, _p(q), _p(k), _p(v), _p(cu), _p(pl), len(cu) - 1, _p(table),
+                                      table.shape[1], scale, _p(out), nthreads or default_threads())
+    if rc != OK:
+        raise ValueError(f"oracle_chunked_prefill rc={rc}")
+    return out
 
 
 def migrate(src: Pool, dst: Pool, layer_begin: int, layer_count: int, src_blocks, dst_blocks,

@@ -373,6 +373,73 @@ int oracle_decode(oracle_pool *p, int32_t layer, const uint16_t *q, const uint16
 }
 
 /* ---------------------------------------------------------------------------
+ * NEXT-3 chunked prefill ("segmenting long prefill into chunks", P:142:
+ * chunk k re-reads the KV of all earlier chunks): sequence r already holds
+ * prefix_lens[r] = c tokens in the pool; its next chunk of l tokens (q,k,v
+ * packed by cu_seqlens) is appended at positions c..c+l-1 and row i (global
+ * position c+i) attends keys 0..c+i. The plain definition, with the keys
+ * gathered through the block table.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  oracle_pool *p;
+  int32_t layer;
+  const uint16_t *q;
+  const int32_t *cu, *prefix, *table;
+  int32_t max_blocks;
+  double scale;
+  double *out;
+} chunk_ctx;
+
+static void chunk_item(void *pctx, long item) {
+  chunk_ctx *c = (chunk_ctx *)pctx;
+  oracle_pool *p = c->p;
+  int n = p->heads, d = p->head_dim, bs = p->block_size;
+  long r = item / n;
+  int h = (int)(item % n);
+  int32_t start = c->cu[r], len = c->cu[r + 1] - c->cu[r], c0 = c->prefix[r];
+  int32_t total = c0 + len;
+  const uint16_t **kr = malloc(sizeof(*kr) * (total > 0 ? total : 1));
+  const uint16_t **vr = malloc(sizeof(*vr) * (total > 0 ? total : 1));
+  double *x = malloc(sizeof(double) * (total > 0 ? total : 1));
+  for (int j = 0; j < total; ++j) {
+    int32_t blk = c->table[(size_t)r * c->max_blocks + j / bs];
+    kr[j] = oracle_pool_page(p, c->layer, 0, blk, h) + (size_t)(j % bs) * d;
+    vr[j] = oracle_pool_page(p, c->layer, 1, blk, h) + (size_t)(j % bs) * d;
+  }
+  for (int i = 0; i < len; ++i)
+    attend_row(c->q + ((size_t)(start + i) * n + h) * d, kr, vr, c0 + i + 1, d, c->scale, x,
+               c->out + ((size_t)(start + i) * n + h) * d);
+  free(kr);
+  free(vr);
+  free(x);
+}
+
+int oracle_chunked_prefill(oracle_pool *p, int32_t layer, const uint16_t *q, const uint16_t *k,
+                           const uint16_t *v, const int32_t *cu_seqlens, const int32_t *prefix_lens,
+                           int32_t num_seqs, const int32_t *table, int32_t max_blocks, double scale,
+                           double *out, int32_t nthreads) {
+  int n = p->heads, d = p->head_dim, bs = p->block_size;
+  if (num_seqs < 0 || layer < 0 || layer >= p->layers) return OR_INVALID;
+  for (int r = 0; r < num_seqs; ++r) { /* append the chunk's K/V at positions c..c+l-1 */
+    int32_t start = cu_seqlens[r], len = cu_seqlens[r + 1] - cu_seqlens[r], c0 = prefix_lens[r];
+    if (c0 < 0 || len < 0 || (c0 + len + bs - 1) / bs > max_blocks) return OR_INVALID;
+    for (int t = 0; t < len; ++t) {
+      int32_t pos = c0 + t, blk = table[(size_t)r * max_blocks + pos / bs];
+      if (blk < 0 || blk >= p->num_blocks) return OR_INVALID;
+      for (int h = 0; h < n; ++h) {
+        memcpy(oracle_pool_page(p, layer, 0, blk, h) + (size_t)(pos % bs) * d,
+               k + ((size_t)(start + t) * n + h) * d, sizeof(uint16_t) * d);
+        memcpy(oracle_pool_page(p, layer, 1, blk, h) + (size_t)(pos % bs) * d,
+               v + ((size_t)(start + t) * n + h) * d, sizeof(uint16_t) * d);
+      }
+    }
+  }
+  chunk_ctx c = {p, layer, q, cu_seqlens, prefix_lens, table, max_blocks, scale, out};
+  parallel_for(chunk_item, &c, (long)num_seqs * n, nthreads);
+  return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
  * a4+a5+a6: migrate whole pages of `num_blocks` logical blocks, layers
  * [layer_begin, layer_begin+layer_count), heads [src_head0, src_head0+head_count)
  * of the source pool into heads [dst_head0, ...) of the destination pool, block

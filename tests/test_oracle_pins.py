@@ -315,3 +315,32 @@ def test_max_rel_err_metric(oracle_mod):
     r = np.array([[1.0, -2.0, 0.5], [0.0, 0.0, 0.0]])
     g = r + np.array([[0.02, 0.0, 0.0], [1e-7, 0.0, 0.0]])
     assert oracle_mod.max_rel_err(g, r) == pytest.approx(0.1)  # 1e-7 / 1e-6 floor
+
+
+# ----------------------------------------------------------------------------
+# NEXT-3 chunked prefill over a paged prefix
+# ----------------------------------------------------------------------------
+@pytest.mark.parametrize("chunks", [[(0, 30)], [(17, 20), (0, 5), (64, 1)], [(100, 37), (3, 3)]])
+def test_chunked_prefill_equals_rows_of_full_prefill(oracle_mod, chunks):
+    """chunk (c, l) of a sequence == rows c..c+l-1 of plain prefill over c+l tokens."""
+    n, d = 2, 64
+    full = syn.prefill_batch(53, [c + l for c, l in chunks], n, d)
+    pool = oracle_mod.Pool(1, 64, n, d)
+    B = len(chunks)
+    table = np.full((B, 16), -1, np.int32)
+    pref = [c for c, _ in chunks]
+    assert pool.append([0] * B, pref, table) == 0
+    hist = [np.arange(full.cu_seqlens[i], full.cu_seqlens[i] + c) for i, (c, _) in enumerate(chunks)]
+    idx = np.concatenate(hist).astype(np.int64) if any(pref) else np.zeros(0, np.int64)
+    pool.write_prefill(0, full.k[idx], full.v[idx], syn.cu_seqlens(pref), table)
+    assert pool.append(pref, [l for _, l in chunks], table) == 0
+    cidx = np.concatenate([np.arange(full.cu_seqlens[i] + c, full.cu_seqlens[i + 1])
+                           for i, (c, _) in enumerate(chunks)]).astype(np.int64)
+    out = oracle_mod.chunked_prefill(pool, 0, full.q[cidx], full.k[cidx], full.v[cidx],
+                                     syn.cu_seqlens([l for _, l in chunks]), pref, table, 0.125)
+    ref = oracle_mod.prefill(full.q, full.k, full.v, full.cu_seqlens, 0.125)[cidx]
+    assert np.abs(out - ref).max() <= 1e-12
+    # the chunk's K/V landed at positions c..c+l-1
+    for i, (c, l) in enumerate(chunks):
+        for t in range(c, c + l):
+            assert np.array_equal(pool.page(0, 0, table[i, t // BS], 1)[t % BS], full.k[full.cu_seqlens[i] + t, 1])
