@@ -138,6 +138,27 @@ ds_status ds_prefill_attn(const void *q, const void *k, const void *v, void *out
                           float softmax_scale, void *stream);
 
 /* ======================================================================
+ * NEXT-3 — chunked prefill over a paged prefix, the technique the
+ * paper contrasts with disaggregation ("segmenting long prefill into
+ * chunks": chunk k re-reads the KV of all earlier chunks). Sequence r
+ * already holds c_r = prefix_lens[r] tokens in the pool; its next chunk of l_r
+ * tokens (q, k, v packed by cu_seqlens) is attended and appended:
+ *   out[i] = sum_{j <= c_r + i} softmax_j(scale * q[i].key[j]) value[j]
+ * with keys/values j < c_r read from the pages (block_table) and j >= c_r the
+ * chunk's own; then cache[...][pos = c_r + t] = k[t], v[t]. With every c_r = 0
+ * this is ds_prefill_attn. The block table must already hold the pages of
+ * positions [0, c_r + l_r). prefix_lens: device int32 [num_seqs];
+ * max_prefix_len / max_chunk_len: host bounds. Two launches (attention, then
+ * the page append of the chunk). Errors as ds_prefill_attn.
+ * ==================================================================== */
+ds_status ds_prefill_attn_chunked(const void *q, const void *k, const void *v, void *out,
+                                  const int32_t *cu_seqlens, const int32_t *prefix_lens,
+                                  int32_t num_seqs, int32_t total_tokens, int32_t max_chunk_len,
+                                  int32_t max_prefix_len, const ds_kv_cache *cache, int32_t layer,
+                                  const int32_t *block_table, int32_t max_blocks_per_seq,
+                                  float softmax_scale, void *stream);
+
+/* ======================================================================
  * a7 + a8 — one decode step of one layer ("generates subsequent tokens
  * one at a time"; P:237 batching; P:696-698 memory-bound decode attention).
  * Reading R9: the new token's K/V are appended at position c = cache_lens[b]

@@ -31,7 +31,7 @@ EXPORTED = (
     "ds_kv_staging_bytes", "ds_kv_pack", "ds_kv_unpack", "ds_comm_get_unique_id", "ds_comm_init",
     "ds_comm_destroy", "ds_kv_migrate_staging_bytes", "ds_kv_migrate", "ds_ipc_export_mem", "ds_ipc_open_mem",
     "ds_ipc_close_mem", "ds_event_create_ipc", "ds_event_open_ipc", "ds_event_record", "ds_event_wait",
-    "ds_event_destroy",
+    "ds_event_destroy", "ds_prefill_attn_chunked",
 )
 
 
@@ -49,7 +49,7 @@ class ds_kv_cache(ctypes.Structure):
 
 def _load():
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2401_09670_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: run `python paper_2401_09670_b200/build.py` "
                           "(there is no fallback implementation)")
     lib = ctypes.CDLL(LIB_PATH)
     P, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
@@ -62,6 +62,8 @@ def _load():
         "ds_pool_num_free": ([P, ctypes.POINTER(i32)], ctypes.c_int),
         "ds_block_table": ([P, i32, i32, P, P, P, i32, i32, ctypes.POINTER(i32)], ctypes.c_int),
         "ds_prefill_attn": ([P, P, P, P, P, i32, i32, i32, cache_p, i32, P, i32, f32, P], ctypes.c_int),
+        "ds_prefill_attn_chunked": ([P, P, P, P, P, P, i32, i32, i32, i32, cache_p, i32, P, i32, f32, P],
+                                    ctypes.c_int),
         "ds_decode_workspace_bytes": ([i32, i32, i32, i32], sz),
         "ds_decode_attn": ([P, P, P, P, cache_p, i32, P, i32, P, i32, i32, f32, P, sz, P], ctypes.c_int),
         "ds_kv_staging_bytes": ([cache_p, i32, i32, i32], sz),
@@ -233,6 +235,25 @@ def ds_prefill_attn(q, k, v, out, cu_seqlens, max_seqlen: int, cache: KVCache, l
                                 cu_seqlens.data_ptr(), cu_seqlens.numel() - 1, T, max_seqlen,
                                 cache.ref(), layer, block_table.data_ptr(), block_table.shape[1],
                                 softmax_scale, _stream(stream)))
+
+
+def ds_prefill_attn_chunked(q, k, v, out, cu_seqlens, prefix_lens, max_chunk_len: int, max_prefix_len: int,
+                            cache: KVCache, layer: int, block_table, softmax_scale: float, stream=None):
+    """NEXT-3: attend each sequence's next chunk over its cached prefix + itself,
+    then append the chunk's K/V to the pages."""
+    torch = _torch()
+    for t, nm in ((q, "q"), (k, "k"), (v, "v"), (out, "out")):
+        _dev(t, torch.bfloat16, nm)
+    _dev(cu_seqlens, torch.int32, "cu_seqlens")
+    _dev(prefix_lens, torch.int32, "prefix_lens")
+    _dev(block_table, torch.int32, "block_table")
+    if q.dim() != 3 or q.shape[1] != cache.heads or q.shape[2] != cache.head_dim:
+        raise ValueError("q must be [T][n_loc][head_dim] matching the cache")
+    _check(_lib.ds_prefill_attn_chunked(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                        cu_seqlens.data_ptr(), prefix_lens.data_ptr(), cu_seqlens.numel() - 1,
+                                        q.shape[0], max_chunk_len, max_prefix_len, cache.ref(), layer,
+                                        block_table.data_ptr(), block_table.shape[1], softmax_scale,
+                                        _stream(stream)))
 
 
 # --------------------------------------------------------------------- a7 + a8

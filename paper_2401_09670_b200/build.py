@@ -1,6 +1,7 @@
 """Build libds.so in-tree with nvcc for sm_100a (no JIT, no torch extension).
 
-    python -m paper_2401_09670_b200.build [--force]
+    python paper_2401_09670_b200/build.py [--force]     (a script: importing the
+    package would load the library this builds)
 
 Links the NCCL that ships with torch (one NCCL per process) and the CUDA
 runtime statically; the driver entry point for TMA descriptors is resolved at

@@ -157,6 +157,7 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
   PrefillArgs a{};
   a.out = out;
   a.cu_seqlens = cu_seqlens;
+  a.prefix_lens = nullptr;
   a.block_table = block_table;
   a.num_seqs = num_seqs;
   a.n_loc = n;
@@ -166,6 +167,68 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
   a.num_blocks = cache->num_blocks;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
   cudaError_t e = launch_prefill(a, tq, tk, tv, tc, D, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, W);
+  return DS_OK;
+}
+
+extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const void *v, void *out,
+                                             const int32_t *cu_seqlens, const int32_t *prefix_lens,
+                                             int32_t num_seqs, int32_t total_tokens, int32_t max_chunk_len,
+                                             int32_t max_prefix_len, const ds_kv_cache *cache, int32_t layer,
+                                             const int32_t *block_table, int32_t max_blocks_per_seq,
+                                             float softmax_scale, void *stream) {
+  const char *W = "ds_prefill_attn_chunked";
+  if (num_seqs < 0) return fail(DS_ERR_INVALID_ARG, "%s: num_seqs < 0", W);
+  if (ds_status s = check_cache(cache, W)) return s;
+  if (num_seqs == 0) return DS_OK;
+  if (!q || !k || !v || !out || !cu_seqlens || !prefix_lens || !block_table)
+    return fail(DS_ERR_INVALID_ARG, "%s: NULL pointer argument", W);
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out))
+    return fail(DS_ERR_INVALID_ARG, "%s: q/k/v/out must be 16-B aligned", W);
+  if (total_tokens < num_seqs || max_chunk_len < 1 || max_chunk_len > total_tokens || max_prefix_len < 0)
+    return fail(DS_ERR_INVALID_ARG, "%s: bad lengths", W);
+  if (layer < 0 || layer >= cache->num_layers) return fail(DS_ERR_INVALID_ARG, "%s: layer out of range", W);
+  if ((max_prefix_len + max_chunk_len + 15) / 16 > max_blocks_per_seq)
+    return fail(DS_ERR_INVALID_ARG, "%s: prefix + chunk needs more than max_blocks_per_seq pages", W);
+  if (!(softmax_scale > 0.f) || !isfinite(softmax_scale))
+    return fail(DS_ERR_INVALID_ARG, "%s: softmax_scale must be finite and > 0", W);
+  if (ds_status s = require_sm100(W)) return s;
+  const int D = cache->head_dim, n = cache->num_heads;
+  CUtensorMap tq, tk, tv, tc;
+  if (ds_status s = qkv_map(&tq, q, total_tokens, n, D, kPrefillQRows, W)) return s;
+  if (ds_status s = qkv_map(&tk, k, total_tokens, n, D, kPrefillKVRows, W)) return s;
+  if (ds_status s = qkv_map(&tv, v, total_tokens, n, D, kPrefillKVRows, W)) return s;
+  if (ds_status s = cache_map(&tc, cache, W)) return s;
+  PrefillArgs a{};
+  a.out = out;
+  a.cu_seqlens = cu_seqlens;
+  a.prefix_lens = prefix_lens;
+  a.block_table = block_table;
+  a.num_seqs = num_seqs;
+  a.n_loc = n;
+  a.max_blocks = max_blocks_per_seq;
+  a.num_q_tiles = (max_chunk_len + 127) / 128;
+  a.layer = layer;
+  a.num_blocks = cache->num_blocks;
+  a.scale_log2 = softmax_scale * 1.4426950408889634f;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = launch_prefill(a, tq, tk, tv, tc, D, st);  // reads the prefix pages + the chunk
+  if (e != cudaSuccess) return cuda_fail(e, W);
+  KvAppendArgs ap{};  // then the chunk's K/V join the pages (positions prefix + t)
+  ap.k = static_cast<const uint16_t *>(k);
+  ap.v = static_cast<const uint16_t *>(v);
+  ap.cache = static_cast<uint16_t *>(cache->base);
+  ap.cu_seqlens = cu_seqlens;
+  ap.prefix_lens = prefix_lens;
+  ap.block_table = block_table;
+  ap.num_seqs = num_seqs;
+  ap.n_loc = n;
+  ap.head_dim = D;
+  ap.max_blocks = max_blocks_per_seq;
+  ap.layer = layer;
+  ap.num_blocks = cache->num_blocks;
+  ap.total_tokens = total_tokens;
+  e = launch_kv_append(ap, st);
   if (e != cudaSuccess) return cuda_fail(e, W);
   return DS_OK;
 }

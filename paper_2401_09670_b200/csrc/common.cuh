@@ -104,6 +104,14 @@ DS_DEVICE void tma_load_3d(void *smem_dst, const void *desc, uint64_t *bar, int 
       "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+DS_DEVICE void tma_load_4d(void *smem_dst, const void *desc, uint64_t *bar, int c0, int c1, int c2,
+                           int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 DS_DEVICE void tma_store_4d(const void *desc, const void *smem_src, int c0, int c1, int c2,
                             int c3) {
   asm volatile(

@@ -53,6 +53,7 @@ constexpr int kPrefillKVRows = 64;  // keys per kv tile (TMA box of K and V)
 struct PrefillArgs {
   void *out;                   // bf16 [T][n][D]
   const int32_t *cu_seqlens;   // [B+1]
+  const int32_t *prefix_lens;  // [B] cached tokens before the chunk (chunked prefill) or nullptr
   const int32_t *block_table;  // [B][max_blocks]
   int32_t num_seqs, n_loc, max_blocks, num_q_tiles;
   int32_t layer, num_blocks;   // cache layer / pool pages
@@ -62,5 +63,14 @@ cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const 
                            const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
                            cudaStream_t stream);
 size_t prefill_smem_bytes(int head_dim);
+
+// NEXT-3: append the chunk's K/V at positions prefix_lens[r] + t of each sequence
+struct KvAppendArgs {
+  const uint16_t *k, *v;       // [T][n][D]
+  uint16_t *cache;             // pool base
+  const int32_t *cu_seqlens, *prefix_lens, *block_table;
+  int32_t num_seqs, n_loc, head_dim, max_blocks, layer, num_blocks, total_tokens;
+};
+cudaError_t launch_kv_append(const KvAppendArgs &a, cudaStream_t stream);
 
 }  // namespace ds

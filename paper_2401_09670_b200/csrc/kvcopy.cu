@@ -99,7 +99,43 @@ __global__ void __launch_bounds__(kThreads) kv_local_kernel(const KvLocalArgs a)
   }
 }
 
+// NEXT-3: scatter the chunk's K/V rows to their pages (position prefix + t);
+// one thread per 16-B vector of (token, kv, head) rows, coalesced along head_dim.
+__global__ void __launch_bounds__(kThreads) kv_append_kernel(const KvAppendArgs a) {
+  const int vec_per_row = a.head_dim / 8;
+  const int64_t per_token = 2LL * a.n_loc * vec_per_row;
+  const int64_t total = (int64_t)a.total_tokens * per_token;
+  const int64_t page_elems = 16LL * a.head_dim;
+  const int64_t kv_stride = (int64_t)a.num_blocks * a.n_loc * page_elems;
+  for (int64_t x = (int64_t)blockIdx.x * kThreads + threadIdx.x; x < total; x += (int64_t)gridDim.x * kThreads) {
+    const int t = (int)(x / per_token);
+    const int64_t rem = x % per_token;
+    const int kv = (int)(rem / (a.n_loc * vec_per_row));
+    const int h = (int)(rem / vec_per_row % a.n_loc), vec = (int)(rem % vec_per_row);
+    int lo = 0, hi = a.num_seqs - 1;  // sequence r with cu[r] <= t < cu[r+1]
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.cu_seqlens[mid] <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    const int pos = a.prefix_lens[lo] + (t - a.cu_seqlens[lo]);
+    const int blk = a.block_table[(int64_t)lo * a.max_blocks + (pos >> 4)];
+    const uint16_t *src = (kv ? a.v : a.k) + ((int64_t)t * a.n_loc + h) * a.head_dim + vec * 8;
+    uint16_t *dst = a.cache + (2LL * a.layer + kv) * kv_stride + ((int64_t)blk * a.n_loc + h) * page_elems +
+                    (int64_t)(pos & 15) * a.head_dim + vec * 8;
+    *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(src);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_kv_append(const KvAppendArgs &a, cudaStream_t stream) {
+  const int64_t total = (int64_t)a.total_tokens * 2 * a.n_loc * (a.head_dim / 8);
+  if (total <= 0) return cudaSuccess;
+  const int64_t blocks = (total + kThreads - 1) / kThreads;
+  kv_append_kernel<<<(int)(blocks < 148LL * 16 ? blocks : 148LL * 16), kThreads, 0, stream>>>(a);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_kv_local(const KvLocalArgs &a, cudaStream_t stream) {
   const int64_t row_bytes = 16LL * a.head_dim * 2 * a.head_count;

@@ -57,7 +57,7 @@ struct Smem {
 // barrier indices ([2] = per stage / per S buffer)
 enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_P = 11, B_O = 12 };
 
-template <int D>
+template <int D, bool kChunked>
 __global__ void __launch_bounds__(kThreads, 2)
     prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_cache,
@@ -71,9 +71,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int seq_start = a.cu_seqlens[r];
   const int len = a.cu_seqlens[r + 1] - seq_start;
   if (i * kBM >= len) return;
-  // kv tiles 0 .. 2i+1 (64 keys each); the second diagonal tile is skipped when
-  // it lies wholly past the end of the sequence
-  const int ntiles = 2 * i + 1 + (len - i * kBM > kBN ? 1 : 0);
+  // chunked prefill (NEXT-3): the sequence already holds c0 tokens in the paged
+  // cache; kv tiles [0, npt) are that prefix (read from the pages), tiles
+  // [npt, ntiles) are the chunk's own keys 0 .. 2i+1 (64 keys each; the second
+  // diagonal tile is skipped when it lies wholly past the end of the chunk)
+  const int c0 = kChunked ? a.prefix_lens[r] : 0;
+  const int npt = kChunked ? (c0 + kBN - 1) / kBN : 0;
+  const int ntiles = npt + 2 * i + 1 + (len - i * kBM > kBN ? 1 : 0);
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -108,8 +112,27 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int c = 0; c < kChunks; ++c)
         tma_load_3d(smem + S::Q + c * kChunkBytes128, &tm_q, &bars[B_Q], c * 64, h, seq_start + i * kBM);
+      const int32_t *btr = a.block_table + (size_t)r * a.max_blocks;
       for (int j = 0; j < ntiles; ++j) {
-        const int st = j & 1, kv0 = seq_start + j * kBN;
+        const int st = j & 1;
+        if (kChunked && j < npt) {
+          // prefix tile: up to 4 pages of 16 cached tokens straight from the pool
+          const int p0 = 4 * j, np = min(4, (c0 + 15) / 16 - p0);
+          const uint32_t bytes = (uint32_t)np * 16 * D * 2;
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv) {
+            if (j >= 2) mbar_wait(&bars[(kv ? B_VE : B_KE) + st], ((j >> 1) - 1) & 1);
+            uint64_t *full = &bars[(kv ? B_VF : B_KF) + st];
+            mbar_arrive_expect_tx(full, bytes);
+            for (int p = 0; p < np; ++p)
+#pragma unroll
+              for (int c = 0; c < kChunks; ++c)
+                tma_load_4d(smem + (kv ? S::V0 : S::K0) + st * S::kKVTile + c * kChunkBytes64 + p * 16 * 128,
+                            &tm_cache, full, c * 64, 0, h, (a.layer * 2 + kv) * a.num_blocks + btr[p0 + p]);
+          }
+          continue;
+        }
+        const int kv0 = seq_start + (j - npt) * kBN;
         if (j >= 2) mbar_wait(&bars[B_KE + st], ((j >> 1) - 1) & 1);  // S_{j-2} has consumed K stage
         mbar_arrive_expect_tx(&bars[B_KF + st], S::kKVTile);
 #pragma unroll
@@ -122,9 +145,11 @@ __global__ void __launch_bounds__(kThreads, 2)
           tma_load_3d(smem + S::V0 + st * S::kKVTile + c * kChunkBytes64, &tm_v, &bars[B_VF + st], c * 64, h, kv0);
       }
       // a3: the diagonal K/V tiles 2i (pages 8i..8i+3) and 2i+1 (8i+4..8i+7) -> paged cache
-      const int npg = min(8, (len - i * kBM + 15) >> 4);
-      const int32_t *bt = a.block_table + (size_t)r * a.max_blocks + i * 8;
-      for (int t = 2 * i; t < ntiles; ++t) {
+      // (chunked mode appends the chunk with ds' append kernel instead: the chunk
+      // need not start on a page boundary)
+      const int npg = kChunked ? 0 : min(8, (len - i * kBM + 15) >> 4);
+      const int32_t *bt = btr + i * 8;
+      for (int t = npt + 2 * i; npg > 0 && t < ntiles; ++t) {
         const int st = t & 1;
         mbar_wait(&bars[B_KF + st], (t >> 1) & 1);
         mbar_wait(&bars[B_VF + st], (t >> 1) & 1);
@@ -207,13 +232,16 @@ __global__ void __launch_bounds__(kThreads, 2)
       // row max on the raw scores (scale > 0 preserves order); only the two
       // diagonal tiles are masked (key position > query position)
       float mx = -__int_as_float(0x7f800000);
-      if (j >= 2 * i) {
-        const int kpos0 = j * kBN;
+      // prefix tiles: keys at or beyond c0 are not cached yet (masked); chunk
+      // tiles: causal within the chunk (key position > query position masked)
+      const bool prefix_tail = kChunked && j == npt - 1 && (c0 % kBN) != 0;
+      if (prefix_tail || j - npt >= 2 * i) {
+        const int lim = prefix_tail ? c0 - 1 - j * kBN : q_pos - (j - npt) * kBN;  // last visible column
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            if (kpos0 + cc * 32 + e > q_pos) sr[cc][e] = 0xff800000u;  // -inf
+            if (cc * 32 + e > lim) sr[cc][e] = 0xff800000u;  // -inf
             mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
           }
       } else {
@@ -301,11 +329,21 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
-template <int D>
+template <int D, bool C>
 static cudaError_t set_prefill_smem_once() {
-  static cudaError_t st = cudaFuncSetAttribute(prefill_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static cudaError_t st = cudaFuncSetAttribute(prefill_kernel<D, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)Smem<D>::ALLOC);
   return st;
+}
+
+template <int D, bool C>
+static cudaError_t launch_one(const PrefillArgs &a, const CUtensorMap &tq, const CUtensorMap &tk,
+                              const CUtensorMap &tv, const CUtensorMap &tc, cudaStream_t stream) {
+  cudaError_t e = set_prefill_smem_once<D, C>();
+  if (e != cudaSuccess) return e;
+  prefill_kernel<D, C><<<dim3(a.num_q_tiles, a.n_loc, a.num_seqs), kThreads, Smem<D>::ALLOC, stream>>>(tq, tk, tv,
+                                                                                                       tc, a);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -317,17 +355,12 @@ size_t prefill_smem_bytes(int head_dim) {
 cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
                            const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
                            cudaStream_t stream) {
-  dim3 grid(a.num_q_tiles, a.n_loc, a.num_seqs);
-  const size_t smem = prefill_smem_bytes(head_dim);
-  cudaError_t e;
-  if (head_dim == 128) {
-    if ((e = set_prefill_smem_once<128>()) != cudaSuccess) return e;
-    prefill_kernel<128><<<grid, kThreads, smem, stream>>>(tm_q, tm_k, tm_v, tm_cache, a);
-  } else {
-    if ((e = set_prefill_smem_once<64>()) != cudaSuccess) return e;
-    prefill_kernel<64><<<grid, kThreads, smem, stream>>>(tm_q, tm_k, tm_v, tm_cache, a);
-  }
-  return cudaGetLastError();
+  const bool chunked = a.prefix_lens != nullptr;
+  if (head_dim == 128)
+    return chunked ? launch_one<128, true>(a, tm_q, tm_k, tm_v, tm_cache, stream)
+                   : launch_one<128, false>(a, tm_q, tm_k, tm_v, tm_cache, stream);
+  return chunked ? launch_one<64, true>(a, tm_q, tm_k, tm_v, tm_cache, stream)
+                 : launch_one<64, false>(a, tm_q, tm_k, tm_v, tm_cache, stream);
 }
 
 }  // namespace ds

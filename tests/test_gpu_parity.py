@@ -431,3 +431,64 @@ def test_reshard_tp_pp_mismatch_bit_exact(oracle_mod, prefill, decode):
                         for kv in (0, 1):
                             ref = opool.page(gl, kv, t_o[r, t // BS], gh)[t % BS]
                             assert np.array_equal(bits[ll, kv, tab[r, t // BS], hh, t % BS], ref), (dr, ll, hh, r, t)
+
+
+def _chunked_round(oracle_mod, side, t_ds, t_or, prefix, chunk, n, d, seed):
+    """one chunk per sequence on top of `prefix` cached tokens (GPU vs oracle)"""
+    B = len(prefix)
+    side.append(prefix, chunk, t_ds, t_or)
+    b = syn.prefill_batch(seed, chunk, n, d)
+    out = torch.full((sum(chunk), n, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    scale = 1.0 / math.sqrt(d)
+    ds.ds_prefill_attn_chunked(to_dev(b.q), to_dev(b.k), to_dev(b.v), out, i32(b.cu_seqlens), i32(prefix),
+                               max(chunk), max(prefix), side.cache, 0, i32(t_ds), scale)
+    torch.cuda.synchronize()
+    ref = oracle_mod.chunked_prefill(side.opool, 0, b.q, b.k, b.v, b.cu_seqlens, prefix, t_or, scale)
+    return oracle_mod.max_rel_err(to_f64(out), ref)
+
+
+@pytest.mark.parametrize("prefix,chunk,d", [
+    ([0, 0], [30, 130], 128),                 # no prefix: plain prefill
+    ([16, 17, 100], [1, 30, 64], 128),        # page-aligned and misaligned prefixes
+    ([700, 5, 64], [130, 300, 1], 128),       # several prefix tiles, multi-tile chunks
+    ([33, 250], [77, 129], 64),
+])
+def test_chunked_prefill_parity(oracle_mod, prefix, chunk, d):
+    """NEXT-3: chunk attention over a paged prefix == the plain definition over
+    prefix + chunk (oracle), and the chunk's K/V are appended to the pages."""
+    n = 4
+    B = len(prefix)
+    maxb = _ceil(max(p + c for p, c in zip(prefix, chunk)) + 1, BS)
+    side = Side(oracle_mod, 1, sum(_ceil(p + c, BS) for p, c in zip(prefix, chunk)) + 10, n, d)
+    side.fragment(5, 6)
+    t_ds = np.full((B, maxb), -1, np.int32)
+    t_or = t_ds.copy()
+    # the cached prefix: written by a plain prefill of the first tokens
+    side.append([0] * B, prefix, t_ds, t_or)
+    if max(prefix) > 0:
+        idx = [i for i, p in enumerate(prefix) if p > 0]
+        pb = syn.prefill_batch(7, [prefix[i] for i in idx], n, d)
+        o = torch.empty((sum(prefix), n, d), dtype=torch.bfloat16, device="cuda")
+        sub = np.ascontiguousarray(t_ds[idx])
+        ds.ds_prefill_attn(to_dev(pb.q), to_dev(pb.k), to_dev(pb.v), o, i32(pb.cu_seqlens), max(prefix), side.cache,
+                           0, i32(sub), 1.0 / math.sqrt(d))
+        side.opool.write_prefill(0, pb.k, pb.v, pb.cu_seqlens, np.ascontiguousarray(t_or[idx]))
+    err = _chunked_round(oracle_mod, side, t_ds, t_or, prefix, chunk, n, d, seed=11)
+    assert err <= TOL and err <= WARN_PREFILL, err
+    total = [p + c for p, c in zip(prefix, chunk)]
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, total, t_ds)
+
+
+def test_chunked_prefill_three_chunks_reread_the_prefix(oracle_mod):
+    """chunk k re-reads the KV of all earlier chunks — three successive
+    chunks of two long prompts, compared after each chunk."""
+    n, d = 8, 128
+    side = Side(oracle_mod, 1, 200, n, d)
+    t_ds = np.full((2, 120), -1, np.int32)
+    t_or = t_ds.copy()
+    done = [0, 0]
+    for k, chunk in enumerate(([512, 300], [512, 300], [200, 457])):
+        err = _chunked_round(oracle_mod, side, t_ds, t_or, done, list(chunk), n, d, seed=20 + k)
+        assert err <= TOL and err <= WARN_PREFILL, (k, err)
+        done = [a + b for a, b in zip(done, chunk)]
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, done, t_ds)
