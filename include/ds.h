@@ -148,13 +148,13 @@ ds_status ds_prefill_attn(const void *q, const void *k, const void *v, void *out
  * chunk's own; then cache[...][pos = c_r + t] = k[t], v[t]. With every c_r = 0
  * this is ds_prefill_attn. The block table must already hold the pages of
  * positions [0, c_r + l_r). prefix_lens: device int32 [num_seqs];
- * max_prefix_len / max_chunk_len: host bounds. Two launches (attention, then
+ * max_chunk_len >= every l_r and max_context_len >= every c_r + l_r: host bounds. Two launches (attention, then
  * the page append of the chunk). Errors as ds_prefill_attn.
  * ==================================================================== */
 ds_status ds_prefill_attn_chunked(const void *q, const void *k, const void *v, void *out,
                                   const int32_t *cu_seqlens, const int32_t *prefix_lens,
                                   int32_t num_seqs, int32_t total_tokens, int32_t max_chunk_len,
-                                  int32_t max_prefix_len, const ds_kv_cache *cache, int32_t layer,
+                                  int32_t max_context_len, const ds_kv_cache *cache, int32_t layer,
                                   const int32_t *block_table, int32_t max_blocks_per_seq,
                                   float softmax_scale, void *stream);
 

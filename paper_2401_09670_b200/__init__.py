@@ -237,7 +237,7 @@ def ds_prefill_attn(q, k, v, out, cu_seqlens, max_seqlen: int, cache: KVCache, l
                                 softmax_scale, _stream(stream)))
 
 
-def ds_prefill_attn_chunked(q, k, v, out, cu_seqlens, prefix_lens, max_chunk_len: int, max_prefix_len: int,
+def ds_prefill_attn_chunked(q, k, v, out, cu_seqlens, prefix_lens, max_chunk_len: int, max_context_len: int,
                             cache: KVCache, layer: int, block_table, softmax_scale: float, stream=None):
     """NEXT-3: attend each sequence's next chunk over its cached prefix + itself,
     then append the chunk's K/V to the pages."""
@@ -251,7 +251,7 @@ def ds_prefill_attn_chunked(q, k, v, out, cu_seqlens, prefix_lens, max_chunk_len
         raise ValueError("q must be [T][n_loc][head_dim] matching the cache")
     _check(_lib.ds_prefill_attn_chunked(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                         cu_seqlens.data_ptr(), prefix_lens.data_ptr(), cu_seqlens.numel() - 1,
-                                        q.shape[0], max_chunk_len, max_prefix_len, cache.ref(), layer,
+                                        q.shape[0], max_chunk_len, max_context_len, cache.ref(), layer,
                                         block_table.data_ptr(), block_table.shape[1], softmax_scale,
                                         _stream(stream)))
 

@@ -174,7 +174,7 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
 extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const void *v, void *out,
                                              const int32_t *cu_seqlens, const int32_t *prefix_lens,
                                              int32_t num_seqs, int32_t total_tokens, int32_t max_chunk_len,
-                                             int32_t max_prefix_len, const ds_kv_cache *cache, int32_t layer,
+                                             int32_t max_context_len, const ds_kv_cache *cache, int32_t layer,
                                              const int32_t *block_table, int32_t max_blocks_per_seq,
                                              float softmax_scale, void *stream) {
   const char *W = "ds_prefill_attn_chunked";
@@ -185,10 +185,10 @@ extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const
     return fail(DS_ERR_INVALID_ARG, "%s: NULL pointer argument", W);
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out))
     return fail(DS_ERR_INVALID_ARG, "%s: q/k/v/out must be 16-B aligned", W);
-  if (total_tokens < num_seqs || max_chunk_len < 1 || max_chunk_len > total_tokens || max_prefix_len < 0)
+  if (total_tokens < num_seqs || max_chunk_len < 1 || max_chunk_len > total_tokens || max_context_len < max_chunk_len)
     return fail(DS_ERR_INVALID_ARG, "%s: bad lengths", W);
   if (layer < 0 || layer >= cache->num_layers) return fail(DS_ERR_INVALID_ARG, "%s: layer out of range", W);
-  if ((max_prefix_len + max_chunk_len + 15) / 16 > max_blocks_per_seq)
+  if ((max_context_len + 15) / 16 > max_blocks_per_seq)
     return fail(DS_ERR_INVALID_ARG, "%s: prefix + chunk needs more than max_blocks_per_seq pages", W);
   if (!(softmax_scale > 0.f) || !isfinite(softmax_scale))
     return fail(DS_ERR_INVALID_ARG, "%s: softmax_scale must be finite and > 0", W);

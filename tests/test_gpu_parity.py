@@ -441,7 +441,7 @@ def _chunked_round(oracle_mod, side, t_ds, t_or, prefix, chunk, n, d, seed):
     out = torch.full((sum(chunk), n, d), float("nan"), dtype=torch.bfloat16, device="cuda")
     scale = 1.0 / math.sqrt(d)
     ds.ds_prefill_attn_chunked(to_dev(b.q), to_dev(b.k), to_dev(b.v), out, i32(b.cu_seqlens), i32(prefix),
-                               max(chunk), max(prefix), side.cache, 0, i32(t_ds), scale)
+                               max(chunk), max(p + c for p, c in zip(prefix, chunk)), side.cache, 0, i32(t_ds), scale)
     torch.cuda.synchronize()
     ref = oracle_mod.chunked_prefill(side.opool, 0, b.q, b.k, b.v, b.cu_seqlens, prefix, t_or, scale)
     return oracle_mod.max_rel_err(to_f64(out), ref)
