@@ -53,6 +53,41 @@ def prefill_point(lens, n, d, reps=20, rot=4):
             "hbm_GBps_algorithmic": byts / t / 1e9}
 
 
+def chunked_point(prefix, chunk, B, n, d, reps=20, rot=4):
+    """NEXT-3: one chunk of `chunk` tokens per sequence on top of `prefix` cached tokens."""
+    T = B * chunk
+    bufs = [[torch.randn((T, n, d), device="cuda", dtype=torch.bfloat16) for _ in range(3)] for _ in range(rot)]
+    out = torch.empty((T, n, d), device="cuda", dtype=torch.bfloat16)
+    pages = B * -(-(prefix + chunk) // 16)
+    cache = ds.KVCache.empty(1, pages + 8, n, d)
+    cache.tensor.normal_()
+    pool = ds.Pool(pages + 8)
+    tab = np.full((B, -(-(prefix + chunk) // 16)), -1, np.int32)
+    ds.ds_block_table(pool, ds.DS_BT_APPEND, [0] * B, [prefix + chunk] * B, tab)
+    tab_d = torch.from_numpy(tab).cuda()
+    cu = torch.from_numpy(np.arange(0, T + 1, chunk).astype(np.int32)).cuda()
+    pl = torch.full((B,), prefix, dtype=torch.int32, device="cuda")
+    scale = 1 / math.sqrt(d)
+    run = lambda r: ds.ds_prefill_attn_chunked(bufs[r % rot][0], bufs[r % rot][1], bufs[r % rot][2], out, cu, pl,
+                                               chunk, prefix + chunk, cache, 0, tab_d, scale)  # noqa: E731
+    for r in range(3):
+        run(r)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for r in range(reps):
+        run(r)
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps / 1e3
+    flops = B * n * 2 * d * chunk * (2 * prefix + chunk + 1)
+    byts = B * n * d * (12 * chunk + 4 * prefix)
+    roof = max(flops / (PEAKS["bf16_tflops"] * 1e12), byts / (PEAKS["hbm_gbs"] * 1e9))
+    return {"kind": "chunked_prefill", "B": B, "prefix": prefix, "chunk": chunk, "n": n, "d": d, "us": t * 1e6,
+            "tflops": flops / t / 1e12, "frac_tensor_peak": flops / t / 1e12 / PEAKS["bf16_tflops"],
+            "frac_attainable": roof / t}
+
+
 def decode_point(B, ctx, n, d, layers=8, reps=5):
     pages_per = -(-(ctx + 2) // 16)
     nb = B * pages_per + 8
@@ -92,13 +127,16 @@ def decode_point(B, ctx, n, d, layers=8, reps=5):
 
 def main():
     p = argparse.ArgumentParser()
-    p.add_argument("--what", default="both")
+    p.add_argument("--what", default="both", help="both | prefill | chunked | decode")
     p.add_argument("--n", type=int, default=40)
     p.add_argument("--d", type=int, default=128)
     a = p.parse_args()
     if a.what in ("both", "prefill"):
         for lens in ([512] * 16, [512] * 64, [128] * 64, [1024] * 8, [2048] * 4, [2048] * 16, [4096] * 4):
             print(json.dumps(prefill_point(lens, a.n, a.d)), flush=True)
+    if a.what in ("both", "chunked"):
+        for prefix in (0, 512, 1024, 1536):
+            print(json.dumps(chunked_point(prefix, 512, 16, a.n, a.d)), flush=True)
     if a.what in ("both", "decode"):
         for B in (1, 8, 16, 32, 64, 128, 256):
             print(json.dumps(decode_point(B, 544, a.n, a.d)), flush=True)
