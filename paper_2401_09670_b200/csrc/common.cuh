@@ -40,6 +40,27 @@ DS_DEVICE float ex2(float x) {
   return y;
 }
 
+// Packed fp32x2 arithmetic (sm_100: FFMA2 / FADD2 issue two lanes of work per
+// instruction slot).
+DS_DEVICE uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+DS_DEVICE void f2_unpack(uint64_t v, float &lo, float &hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+DS_DEVICE uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+DS_DEVICE uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 // 2^x on the FMA pipe (offloads the MUFU unit, whose 16 ex2/clk/SM equal the
 // tensor pipe's demand in attention softmax). Cody-Waite split x = n + f with
 // n = rint(x) (magic-number add), f in [-0.5, 0.5], 2^f by a degree-3 minimax

@@ -262,20 +262,24 @@ __global__ void __launch_bounds__(kThreads, 2)
       // p = 2^(s*scale*log2e - m): one FFMA + one MUFU ex2 per element; P is
       // rounded to bf16 (the P operand of the P.V MMA), the row sum stays fp32.
       uint32_t pk[32];
-      float rs0 = 0.f, rs1 = 0.f;
+      const uint64_t sl2x2 = f2_pack(sl2, sl2), negm2 = f2_pack(-m_new, -m_new);
+      uint64_t rs2 = f2_pack(0.f, 0.f);
 #pragma unroll
       for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          // kPolyEvery-th exponentials on the FMA pipe, the rest on MUFU
-          const float x0 = fmaf(__uint_as_float(sr[cc][e]), sl2, -m_new);
-          const float x1 = fmaf(__uint_as_float(sr[cc][e + 1]), sl2, -m_new);
+          // exponent arguments two at a time (FFMA2); kPolyEvery-th exponentials on
+          // the FMA pipe, the rest on MUFU; the fp32 row sum two at a time (FADD2)
+          float x0, x1;
+          f2_unpack(f2_fma(f2_pack(__uint_as_float(sr[cc][e]), __uint_as_float(sr[cc][e + 1])), sl2x2, negm2), x0,
+                    x1);
           const float p0 = (e % kPolyEvery) == 0 ? ex2_poly(x0) : ex2(x0);
           const float p1 = ((e + 1) % kPolyEvery) == 0 ? ex2_poly(x1) : ex2(x1);
-          rs0 += p0;
-          rs1 += p1;
+          rs2 = f2_add(rs2, f2_pack(p0, p1));
           pk[cc * 16 + e / 2] = pack_bf16(p0, p1);
         }
+      float rs0, rs1;
+      f2_unpack(rs2, rs0, rs1);
       l = l * alpha + (rs0 + rs1);
       m = m_new;
       if (j > 0 && __any_sync(0xffffffffu, grow)) {  // warp-uniform O rescale, only when a base moved
@@ -286,8 +290,14 @@ __global__ void __launch_bounds__(kThreads, 2)
           uint32_t o[32];
           tmem_ld32(tO + lane_off + cc * 32, o);
           tmem_wait_ld();
+          const uint64_t a2 = f2_pack(alpha, alpha), z2 = f2_pack(0.f, 0.f);
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+          for (int e = 0; e < 32; e += 2) {
+            float lo, hi;
+            f2_unpack(f2_fma(f2_pack(__uint_as_float(o[e]), __uint_as_float(o[e + 1])), a2, z2), lo, hi);
+            o[e] = __float_as_uint(lo);
+            o[e + 1] = __float_as_uint(hi);
+          }
           tmem_st32(tO + lane_off + cc * 32, o);
         }
       }
