@@ -5,6 +5,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -149,10 +150,15 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
     return fail(DS_ERR_INVALID_ARG, "%s: softmax_scale must be finite and > 0", W);
   if (ds_status s = require_sm100(W)) return s;
   const int D = cache->head_dim, n = cache->num_heads;
+  // kernel choice: one 128-row q tile per CTA (2 CTAs/SM) for short prompts, a
+  // ping-pong pair of q tiles per CTA for longer ones; DS_PREFILL_KERNEL=1q|2q overrides
+  static const char *force = getenv("DS_PREFILL_KERNEL");
+  const bool two_q = force ? (strcmp(force, "2q") == 0) : (max_seqlen >= kPrefill2qMinLen);
+  const int kv_rows = two_q ? 128 : kPrefillKVRows;
   CUtensorMap tq, tk, tv, tc;
   if (ds_status s = qkv_map(&tq, q, total_tokens, n, D, kPrefillQRows, W)) return s;
-  if (ds_status s = qkv_map(&tk, k, total_tokens, n, D, kPrefillKVRows, W)) return s;
-  if (ds_status s = qkv_map(&tv, v, total_tokens, n, D, kPrefillKVRows, W)) return s;
+  if (ds_status s = qkv_map(&tk, k, total_tokens, n, D, kv_rows, W)) return s;
+  if (ds_status s = qkv_map(&tv, v, total_tokens, n, D, kv_rows, W)) return s;
   if (ds_status s = cache_map(&tc, cache, W)) return s;
   PrefillArgs a{};
   a.out = out;
@@ -162,11 +168,12 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
   a.num_seqs = num_seqs;
   a.n_loc = n;
   a.max_blocks = max_blocks_per_seq;
-  a.num_q_tiles = (max_seqlen + 127) / 128;
+  a.num_q_tiles = two_q ? (max_seqlen + 255) / 256 : (max_seqlen + 127) / 128;
   a.layer = layer;
   a.num_blocks = cache->num_blocks;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
-  cudaError_t e = launch_prefill(a, tq, tk, tv, tc, D, static_cast<cudaStream_t>(stream));
+  cudaError_t e = two_q ? launch_prefill2q(a, tq, tk, tv, tc, D, static_cast<cudaStream_t>(stream))
+                        : launch_prefill(a, tq, tk, tv, tc, D, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, W);
   return DS_OK;
 }

@@ -63,6 +63,10 @@ cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const 
                            const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
                            cudaStream_t stream);
 size_t prefill_smem_bytes(int head_dim);
+// prompts of >= kPrefill2qMinLen tokens: two 128-row q tiles per CTA, 128-key tiles
+constexpr int kPrefill2qMinLen = 256;
+cudaError_t launch_prefill2q(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
+                             const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim, cudaStream_t stream);
 
 // NEXT-3: append the chunk's K/V at positions prefix_lens[r] + t of each sequence
 struct KvAppendArgs {
