@@ -150,10 +150,11 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
     return fail(DS_ERR_INVALID_ARG, "%s: softmax_scale must be finite and > 0", W);
   if (ds_status s = require_sm100(W)) return s;
   const int D = cache->head_dim, n = cache->num_heads;
-  // kernel choice: one 128-row q tile per CTA (2 CTAs/SM) for short prompts, a
-  // ping-pong pair of q tiles per CTA for longer ones; DS_PREFILL_KERNEL=1q|2q overrides
+  // kernel choice: one 128-row q tile per CTA, two CTAs per SM (measured fastest
+  // at every length, profiles/r01). DS_PREFILL_KERNEL=2q selects the experimental
+  // ping-pong pair-of-q-tiles CTA (prefill2q.cu; parity-tested, slower today).
   static const char *force = getenv("DS_PREFILL_KERNEL");
-  const bool two_q = force ? (strcmp(force, "2q") == 0) : (max_seqlen >= kPrefill2qMinLen);
+  const bool two_q = force && strcmp(force, "2q") == 0;
   const int kv_rows = two_q ? 128 : kPrefillKVRows;
   CUtensorMap tq, tk, tv, tc;
   if (ds_status s = qkv_map(&tq, q, total_tokens, n, D, kPrefillQRows, W)) return s;

@@ -63,8 +63,7 @@ cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const 
                            const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
                            cudaStream_t stream);
 size_t prefill_smem_bytes(int head_dim);
-// prompts of >= kPrefill2qMinLen tokens: two 128-row q tiles per CTA, 128-key tiles
-constexpr int kPrefill2qMinLen = 256;
+// experimental (DS_PREFILL_KERNEL=2q): two 128-row q tiles per CTA, 128-key tiles
 cudaError_t launch_prefill2q(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
                              const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim, cudaStream_t stream);
 

@@ -1,5 +1,8 @@
-// prefill2q.cu — a2 + a3 for longer prompts: one CTA per PAIR of 128-row q
-// tiles (256 query rows) of one (sequence, head), FA4-style ping-pong.
+// prefill2q.cu — EXPERIMENTAL a2 + a3 variant (DS_PREFILL_KERNEL=2q): one CTA
+// per PAIR of 128-row q tiles (256 query rows) of one (sequence, head),
+// FA4-style ping-pong. Parity-tested; measured slower than prefill.cu's two
+// CTAs per SM (profiles/r01: 4x4096 821 us vs 683 us) because P aliases S in
+// TMEM, so S_t(j+1) must wait for P_t(j) V_t(j) and the per-tile chain grows.
 //
 // Same computation as prefill.cu (§2.1, App. A;
 // readings R1, R2; a3 page write P:102):

@@ -492,3 +492,18 @@ def test_chunked_prefill_three_chunks_reread_the_prefix(oracle_mod):
         assert err <= TOL and err <= WARN_PREFILL, (k, err)
         done = [a + b for a, b in zip(done, chunk)]
     assert pages_match(to_bits(side.cache.tensor), side.opool, 0, done, t_ds)
+
+
+def test_experimental_pair_kernel_parity():
+    """DS_PREFILL_KERNEL=2q (prefill2q.cu) is read once per process: run the
+    prefill parity cases in a child process with it set."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DS_PREFILL_KERNEL="2q")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_parity.py"), "-k",
+                        "prefill and not chunked and not experimental"], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
