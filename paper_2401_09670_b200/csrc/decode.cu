@@ -6,7 +6,7 @@
 // at position c before attending, so the step attends c+1 tokens.
 //
 // B200 design (HBM-bound; no tensor cores — every cached element is used once):
-//  * persistent grid of one 8-warp CTA per SM; the (sequence, head, page) space
+//  * persistent grid of one 16-warp CTA per SM; the (sequence, head, page) space
 //    is flattened and cut into equal contiguous page ranges, one per warp, so
 //    every warp streams the same number of pages whatever the batch and length
 //    mix (no wave tail, no idle SMs on ragged batches);
