@@ -293,8 +293,11 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   asm volatile("griddepcontrol.wait;" ::: "memory");
   build_prefix(a.cache_lens, B, prefix);
   const int64_t P = (int64_t)n * prefix[B];
-  const int64_t W = (int64_t)gridDim.x * kWarps;
+  // at most one warp per page: every active warp range is non-empty, so a pair
+  // never spans idle warps (tiny batches would otherwise merge across thousands)
+  const int64_t W = min((int64_t)gridDim.x * kWarps, P);
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  if (gw >= W) return;
   const int64_t x0 = range_begin(gw, W, P), x1 = range_begin(gw + 1, W, P);
   if (x0 >= x1) return;
 
