@@ -73,7 +73,8 @@ def parse():
     p.add_argument("--output", type=int, default=0, help="decode steps override")
     p.add_argument("--impl", default="ds", choices=["ds", "reference"])
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--e2e-steps", type=int, default=6)
+    p.add_argument("--e2e-trace", action="store_true", help="print a per-step copy/compute timeline to stderr")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graphs", action="store_true", help="eager decode launches (no CUDA graphs)")
     p.add_argument("--transport", default="nccl", choices=["nccl", "pull"],
@@ -242,12 +243,15 @@ class Engine:
             self.max_c = w.max_len + w.out_len - 1  # largest cache length of the batch (validation only)
             self.ws = torch.zeros(max(16, ds.ds_decode_workspace_bytes(w.B, w.n, w.d, self.max_c)),
                                   dtype=torch.uint8, device=dev)
-            # fixed device block table / lengths read by the captured decode graphs
-            self.dtab = torch.full((w.B, w.maxb), -1, dtype=torch.int32, device=dev)
-            self.dlen = torch.zeros((w.B,), dtype=torch.int32, device=dev)
-            self.h_tab2 = [torch.empty((w.B, w.maxb), dtype=torch.int32).pin_memory() for _ in range(2)]
-            self.h_len2 = [torch.empty((w.B,), dtype=torch.int32).pin_memory() for _ in range(2)]
-            self.h_ev2 = [None, None]
+            # per-step device block tables / lengths read by the captured decode graphs:
+            # the scheduler runs a batch's APPENDs for all its steps up front (fixed output
+            # lengths) and uploads them in one copy, so no small per-step H2D copy queues
+            # behind bulk transfers on the copy engine
+            self.dtab = torch.full((w.out_len, w.B, w.maxb), -1, dtype=torch.int32, device=dev)
+            self.dlen = torch.zeros((w.out_len, w.B), dtype=torch.int32, device=dev)
+            self.h_tab2 = [torch.empty((w.out_len, w.B, w.maxb), dtype=torch.int32).pin_memory() for _ in range(2)]
+            self.h_len2 = [torch.empty((w.out_len, w.B), dtype=torch.int32).pin_memory() for _ in range(2)]
+            self.h_ev2 = [None] * 2
             self.hslot = 0
             self.graphs = None
         nblk = sum(w.pages)
@@ -262,38 +266,64 @@ class Engine:
         self.h_tab = torch.empty((self.ring, w.B, w.maxb), dtype=torch.int32).pin_memory()
         self.d_tab = torch.empty((self.ring, w.B, w.maxb), dtype=torch.int32, device=dev)
         self.h_ev = [None] * self.ring
+        self.d_free = [None] * self.ring  # events: device slot no longer read
         self.slot = 0
+        self.copy_stream = None  # e2e: table uploads share the bulk-copy stream
+        self.dec_free = None  # event: the decode graphs of the last batch are done with dtab/dlen
         self.launches = 0
         self.layer_hook = None  # e2e: per-layer input copies overlapped with the prefill
+        self.step_trace = None  # --e2e-trace: an event after every decode step
         idx = np.concatenate([np.arange(b * w.maxb, b * w.maxb + p) for b, p in enumerate(w.pages)])
         self._idx = _i32(torch, idx).long()
 
     # -- host -> device block tables ------------------------------------------------
+    def _h2d(self, copies, free_ev):
+        """Async H2D of small tables; returns the event that marks their arrival.
+        With copy_stream set (e2e), they ride the same FIFO stream as the bulk input
+        copies: a copy engine serves H2D copies in the order they become ready, so a
+        table upload on another stream would wait behind every bulk copy that became
+        ready first. free_ev: the device buffer may be overwritten once it completes."""
+        torch = self.torch
+        if self.copy_stream is None:
+            for dst, src in copies:
+                dst.copy_(src, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            return ev
+        main, cs = torch.cuda.current_stream(), self.copy_stream
+        with torch.cuda.stream(cs):
+            if free_ev is not None:
+                cs.wait_event(free_ev)
+            for dst, src in copies:
+                dst.copy_(src, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        main.wait_event(ev)
+        return ev
+
     def upload(self, table: np.ndarray):
         s = self.slot
         self.slot = (s + 1) % self.ring
+        # every consumer of the previous upload is enqueued by now: its slot is free
+        # once the caller's stream gets here
+        mark = self.torch.cuda.Event()
+        mark.record()
+        self.d_free[(s - 1) % self.ring] = mark
         if self.h_ev[s] is not None:
             self.h_ev[s].synchronize()  # the previous copy out of this slot has completed
         self.h_tab[s].numpy()[:] = table
-        self.d_tab[s].copy_(self.h_tab[s], non_blocking=True)
-        ev = self.torch.cuda.Event()
-        ev.record()
-        self.h_ev[s] = ev
+        self.h_ev[s] = self._h2d([(self.d_tab[s], self.h_tab[s])], self.d_free[s])
         return self.d_tab[s]
 
-    def upload_decode(self, table: np.ndarray, lens):
-        """async H2D of the decode block table + lengths into the graphs' fixed buffers"""
+    def upload_decode(self, tables: np.ndarray, lens: np.ndarray):
+        """one async H2D of a batch's per-step decode tables + lengths into the graphs' buffers"""
         i = self.hslot
         self.hslot ^= 1
         if self.h_ev2[i] is not None:
-            self.h_ev2[i].synchronize()
-        self.h_tab2[i].numpy()[:] = table
+            self.h_ev2[i].synchronize()  # the upload of two batches ago has left this slot
+        self.h_tab2[i].numpy()[:] = tables
         self.h_len2[i].numpy()[:] = lens
-        self.dtab.copy_(self.h_tab2[i], non_blocking=True)
-        self.dlen.copy_(self.h_len2[i], non_blocking=True)
-        ev = self.torch.cuda.Event()
-        ev.record()
-        self.h_ev2[i] = ev
+        self.h_ev2[i] = self._h2d([(self.dtab, self.h_tab2[i]), (self.dlen, self.h_len2[i])], self.dec_free)
 
     def page_ids(self, table_dev):
         """the batch's page ids in logical order (device gather of the table rows)"""
@@ -305,7 +335,7 @@ class Engine:
         w, ds = self.w, self.ds
         for layer in range(w.L):
             ds.ds_decode_attn(self.dq[s, layer], self.dk[s, layer], self.dv[s, layer], self.dout[s], self.D, layer,
-                              self.dtab, self.dlen, self.max_c, w.scale, self.ws)
+                              self.dtab[s], self.dlen[s], self.max_c, w.scale, self.ws)
 
     def capture_decode_graphs(self):
         """one CUDA graph per decode step: the layer loop becomes a single launch"""
@@ -461,15 +491,25 @@ class Engine:
         """a1 (APPEND per step) + a7/a8 for `output` steps, then FREE"""
         ds, w = self.ds, self.w
         cur = list(w.lens)
-        for s in range(w.out_len):
+        tabs = np.empty((w.out_len, w.B, w.maxb), np.int32)
+        lens = np.empty((w.out_len, w.B), np.int32)
+        for s in range(w.out_len):  # a1: one APPEND per step (a page whenever a sequence crosses 16k)
             ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, cur, [1] * w.B, self.td)
-            self.upload_decode(self.td, cur)
+            tabs[s], lens[s] = self.td, cur
+            cur = [c + 1 for c in cur]
+        self.upload_decode(tabs, lens)
+        for s in range(w.out_len):
             if self.graphs is not None:
                 self.graphs[s].replay()
             else:
                 self.decode_layers(s)
+            if self.step_trace is not None:
+                ev = self.torch.cuda.Event(enable_timing=True)
+                ev.record()
+                self.step_trace.append(ev)
             self.launches += w.L  # one decode_kernel per layer (split merge fused)
-            cur = [c + 1 for c in cur]
+        self.dec_free = self.torch.cuda.Event()
+        self.dec_free.record()
         ds.ds_block_table(self.pool_d, ds.DS_BT_FREE, cur, None, self.td)
         self._mark(marks, "decode")
 
@@ -862,19 +902,40 @@ def run_e2e(args, eng, w, world, replicas, torch):
         host["out"] = torch.empty(tuple(eng.dout.shape), dtype=bf).pin_memory()
 
     # host->device copies ride a separate stream so PCIe overlaps the kernels:
-    # layer l's inputs land in rotating buffer l % n_in; the copy of layer l + n_in
-    # waits until the prefill of layer l has consumed that buffer.
+    # layer l's inputs land in rotating buffer l % n_in, and a copy into buffer i
+    # waits only until the prefill that last read buffer i is done — so the next
+    # batch's prompt copies stream in while this batch decodes (PCIe stays busy).
     main, cs = torch.cuda.current_stream(), torch.cuda.Stream()
+    if eng.pf:  # more landing buffers (free HBM permitting) so the copies can run a whole decode ahead
+        per_buf = 3 * eng.q[0].numel() * 2
+        spare = max(0, torch.cuda.mem_get_info()[0] - (12 << 30)) // per_buf
+        for _ in range(min(w.L, 24) - len(eng.q)):
+            if spare <= 0:
+                break
+            for lst in (eng.q, eng.k, eng.v):
+                lst.append(torch.empty_like(lst[0]))
+            spare -= 1
     n_in = len(eng.q) if eng.pf else 0
     copied = [torch.cuda.Event() for _ in range(w.L)]
-    freed = [torch.cuda.Event() for _ in range(w.L)]
+    buf_free = [None] * n_in  # event: the last prefill reading buffer i has finished
+
+    trace = []  # --e2e-trace: (label, event) on the stream that does the work
+    step_traces = []  # --e2e-trace: per batch, decode-step completion times (ms from decode start)
+
+    def tmark(label, stream):
+        if args.e2e_trace:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            trace.append((label, e))
 
     def copy_layer(layer):
         nonlocal h2d
         i = layer % n_in
         with torch.cuda.stream(cs):
-            if layer >= n_in:
-                cs.wait_event(freed[layer - n_in])
+            if buf_free[i] is not None:
+                cs.wait_event(buf_free[i])
+            if layer in (0, w.L - 1):
+                tmark(f"copy{layer}", cs)
             eng.q[i].copy_(host["qkv"][0], non_blocking=True)
             eng.k[i].copy_(host["qkv"][1], non_blocking=True)
             eng.v[i].copy_(host["qkv"][2], non_blocking=True)
@@ -885,12 +946,13 @@ def run_e2e(args, eng, w, world, replicas, torch):
         if when == "before":
             main.wait_event(copied[layer])
         else:
-            freed[layer].record(main)
+            ev = torch.cuda.Event()
+            ev.record(main)
+            buf_free[layer % n_in] = ev
             if layer + n_in < w.L:
                 copy_layer(layer + n_in)
 
     def copy_prefill_inputs():
-        cs.wait_stream(main)  # buffers of the previous batch are consumed in stream order
         for layer in range(min(n_in, w.L)):
             copy_layer(layer)
 
@@ -912,15 +974,23 @@ def run_e2e(args, eng, w, world, replicas, torch):
 
     def decode_after_inputs():
         main.wait_event(dec_ready)
+        tmark("decode", main)
+        if args.e2e_trace:
+            eng.step_trace = []
         eng.decode_batch(None)
+        tmark("decode_end", main)
+        if args.e2e_trace:
+            step_traces.append((trace[-2][1], eng.step_trace))
+            eng.step_trace = None
 
     def step():  # Engine.step with the host <-> device traffic of every batch
         role = eng.role
         eng.layer_hook = hook if eng.pf else None
         if role.phase == "both":
-            decode_io(False)
-            copy_prefill_inputs()
             eng.admit()
+            copy_prefill_inputs()  # prompt copies before the decode inputs: they wait on prefill, not decode
+            decode_io(False)
+            tmark("prefill", main)
             eng.prefill_and_send(0, None)
             decode_after_inputs()
             decode_io(True)
@@ -935,6 +1005,7 @@ def run_e2e(args, eng, w, world, replicas, torch):
             decode_io(True)
         eng.layer_hook = None
 
+    eng.copy_stream = cs
     step()
     torch.cuda.synchronize()
     h2d = d2h = 0
@@ -946,6 +1017,12 @@ def run_e2e(args, eng, w, world, replicas, torch):
     main.wait_stream(cs)
     e1.record()
     torch.cuda.synchronize()
+    eng.copy_stream = None
+    if trace:
+        t0 = trace[0][1]
+        sys.stderr.write("e2e trace (ms): " + " ".join(f"{l}@{t0.elapsed_time(e):.1f}" for l, e in trace) + "\n")
+        for t0, evs in step_traces:
+            sys.stderr.write(f"e2e decode steps (ms): {[round(t0.elapsed_time(e), 1) for e in evs]}\n")
     ms = max_over_ranks(e0.elapsed_time(e1), world) / args.e2e_steps
     if world > 1:  # whole-job host <-> device bytes
         import torch.distributed as dist

@@ -80,27 +80,29 @@ DS_DEVICE int npages_of(int c) { return (c + 1 + 15) >> 4; }
 // page range [B_w, B_{w+1}) of warp w out of W over P pages
 __host__ __device__ inline int64_t range_begin(int64_t w, int64_t W, int64_t P) { return w * P / W; }
 
-// exclusive prefix of pages per sequence: prefix[b] = sum_{b' < b} npages(b')
+// exclusive prefix of pages per sequence: prefix[b] = sum_{b' < b} npages(b').
+// Thread t sums a contiguous run of sequences; the runs are scanned with warp
+// shuffles and one pass over the kWarps warp totals (no serial loop over threads).
 DS_DEVICE void build_prefix(const int32_t *cache_lens, int B, int *prefix) {
-  __shared__ int partial[kWarps * 32];
-  const int T = blockDim.x, t = threadIdx.x;
+  __shared__ int warp_total[kWarps];
+  const int T = blockDim.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int per = (B + T - 1) / T;
   const int b0 = min(B, t * per), b1 = min(B, b0 + per);
   int s = 0;
   for (int b = b0; b < b1; ++b) s += npages_of(cache_lens[b]);
-  partial[t] = s;
-  __syncthreads();
-  if (t == 0) {
-    int run = 0;
-    for (int i = 0; i < T; ++i) {
-      const int v = partial[i];
-      partial[i] = run;
-      run += v;
-    }
-    prefix[B] = run;
+  int inc = s;  // inclusive scan within the warp
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
   }
+  if (lane == 31) warp_total[warp] = inc;
   __syncthreads();
-  int run = partial[t];
+  int base = 0;
+#pragma unroll
+  for (int w = 0; w < kWarps; ++w) base += w < warp ? warp_total[w] : 0;
+  int run = base + inc - s;
+  if (t == T - 1) prefix[B] = base + inc;
   for (int b = b0; b < b1; ++b) {
     prefix[b] = run;
     run += npages_of(cache_lens[b]);
@@ -143,11 +145,21 @@ DS_DEVICE int64_t owner_of(int64_t x, int64_t W, int64_t P) {
   return w;
 }
 
+// partial row of warp w, segment seg (0: its first pair, 1: its last pair):
+// o[D] then m, l; rows padded to 16 B so o loads/stores are vectors
+template <int D>
+constexpr int kPartialStride = D + 4;
+template <int D>
+DS_DEVICE float *partial_row(float *ws, int64_t w, int seg) {
+  return ws + ((size_t)w * 2 + seg) * kPartialStride<D>;
+}
+
 // a8, fused: the warp that publishes the LAST partial of a straddling (seq, head)
 // pair merges all of them (log-sum-exp rule) and resets the pair's ticket:
 //   m* = max_k m_k ; l* = sum_k l_k 2^(m_k - m*) ; o = sum_k o_k 2^(m_k - m*) / l*
 // Partials are published with a release fence + atomic ticket; the merger reads
-// them with an acquire fence through L2 (ld.cg).
+// them with an acquire fence through L2 (ld.cg). Every warp range is non-empty
+// (W <= P), so all k candidate contributors publish one partial each.
 template <int D>
 DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int h, int64_t W, int64_t P,
                              int lane) {
@@ -155,38 +167,33 @@ DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int 
   const int npg = prefix[b + 1] - prefix[b];
   const int64_t start = (int64_t)n * prefix[b] + (int64_t)h * npg;
   const int64_t w0 = owner_of(start, W, P), w1 = owner_of(start + npg - 1, W, P);
-  const int k = (int)(w1 - w0 + 1);  // candidate contributors (empty ranges skipped)
-  // lane j looks at contributors j, j+32, ...: is it non-empty?
-  int need = 0;
-  for (int j = lane; j < k; j += 32) need += range_begin(w0 + j, W, P) < range_begin(w0 + j + 1, W, P);
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) need += __shfl_xor_sync(0xffffffffu, need, o);
+  const int k = (int)(w1 - w0 + 1);
   __syncwarp();  // the partial written by lanes < TPG is ordered before the release below
   int ticket = 0;
   const int pair = b * n + h;
   if (lane == 0)
     asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(ticket) : "l"(a.tickets + pair) : "memory");
   ticket = __shfl_sync(0xffffffffu, ticket, 0);
-  if (ticket != need - 1) return;
+  if (ticket != k - 1) return;
   __syncwarp();
-  const int slot0 = range_begin(w0, W, P) < start ? 1 : 0;  // the pair is w0's last segment
-  constexpr int PER = D / 32;
+  const int seg0 = range_begin(w0, W, P) < start ? 1 : 0;  // the pair is w0's last segment
+  constexpr int PER = D / 32;  // dims per lane: 4 (D = 128) or 2 (D = 64)
+  constexpr int U = 8;         // contributors whose o slices are in flight at once
   float mm = kNegInf, lt = 0.f, ot[PER];
 #pragma unroll
   for (int e = 0; e < PER; ++e) ot[e] = 0.f;
-  for (int j0 = 0; j0 < k; j0 += 32) {  // 32 contributors per round, loads in parallel
+  for (int j0 = 0; j0 < k; j0 += 32) {  // 32 contributors per round, (m, l) loads in parallel
     const int j = j0 + lane;
-    const int64_t w = w0 + j;
-    const bool live = j < k && range_begin(w, W, P) < range_begin(w + 1, W, P);
-    const float *ws = a.workspace + ((size_t)w * 2 + (j == 0 ? slot0 : 0)) * (D + 2);
-    const float mj = live ? __ldcg(ws + D) : kNegInf;
-    const float lj = live ? __ldcg(ws + D + 1) : 0.f;
+    const float *ws = partial_row<D>(a.workspace, w0 + j, j == 0 ? seg0 : 0);
+    const float mj = j < k ? __ldcg(ws + D) : kNegInf;
+    const float lj = j < k ? __ldcg(ws + D + 1) : 0.f;
     float mr = mj;
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) mr = fmaxf(mr, __shfl_xor_sync(0xffffffffu, mr, o));
     const float m_new = fmaxf(mm, mr);
     const float alpha = rescale(mm, m_new);
-    float wj = rescale(mj, m_new), lsum = lj * wj;
+    const float wj = rescale(mj, m_new);
+    float lsum = lj * wj;
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
     lt = lt * alpha + lsum;
@@ -194,12 +201,30 @@ DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int 
     for (int e = 0; e < PER; ++e) ot[e] *= alpha;
     mm = m_new;
     const int cnt = min(32, k - j0);
-    for (int jj = 0; jj < cnt; ++jj) {  // lane-parallel over dims, loads independent across jj
-      const float wt = __shfl_sync(0xffffffffu, wj, jj);
-      if (wt != 0.f) {
-        const float *wsj = a.workspace + ((size_t)(w0 + j0 + jj) * 2 + (j0 + jj == 0 ? slot0 : 0)) * (D + 2);
+    for (int u0 = 0; u0 < cnt; u0 += U) {  // U independent vector loads, then the FMAs
+      float val[U][PER];
 #pragma unroll
-        for (int e = 0; e < PER; ++e) ot[e] = fmaf(__ldcg(wsj + lane * PER + e), wt, ot[e]);
+      for (int u = 0; u < U; ++u) {
+        const int jj = j0 + u0 + u;
+        const float *src = partial_row<D>(a.workspace, w0 + jj, jj == 0 ? seg0 : 0) + lane * PER;
+        if (u0 + u < cnt) {
+          if constexpr (PER == 4) {
+            const float4 f = __ldcg(reinterpret_cast<const float4 *>(src));
+            val[u][0] = f.x; val[u][1] = f.y; val[u][2] = f.z; val[u][3] = f.w;
+          } else {
+            const float2 f = __ldcg(reinterpret_cast<const float2 *>(src));
+            val[u][0] = f.x; val[u][1] = f.y;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < PER; ++e) val[u][e] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float wt = __shfl_sync(0xffffffffu, wj, (u0 + u) & 31);
+#pragma unroll
+        for (int e = 0; e < PER; ++e) ot[e] = fmaf(val[u][e], wt, ot[e]);
       }
     }
   }
@@ -400,10 +425,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
           *reinterpret_cast<uint4 *>(reinterpret_cast<uint16_t *>(a.out) + row) = o;
         }
       } else {  // a straddling pair: partial (o, m, l), merged by the last contributor (a8)
-        float *ws = a.workspace + ((size_t)gw * 2 + (first_seg ? 0 : 1)) * (D + 2);
+        float *ws = partial_row<D>(a.workspace, gw, first_seg ? 0 : 1);
         if (lane < TPG) {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) ws[dpart * 8 + e] = acc[e];
+          reinterpret_cast<float4 *>(ws + dpart * 8)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+          reinterpret_cast<float4 *>(ws + dpart * 8)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
           if (lane == 0) {
             ws[D] = m;
             ws[D + 1] = l;
@@ -426,7 +451,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
 }  // namespace
 
 size_t decode_partials_bytes(int head_dim, int num_sms) {
-  return (size_t)num_sms * kWarps * 2 * (head_dim + 2) * sizeof(float);
+  return (size_t)num_sms * kWarps * 2 * (head_dim + 4) * sizeof(float);  // kPartialStride
 }
 size_t decode_workspace_bytes(int num_seqs, int n_loc, int head_dim, int num_sms) {
   return decode_partials_bytes(head_dim, num_sms) + (size_t)num_seqs * n_loc * 4;  // + tickets

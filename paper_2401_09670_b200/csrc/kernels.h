@@ -17,7 +17,7 @@ struct DecodeArgs {
   const uint16_t *cache;              // pool base [L][2][NB][n][16][D]
   const int32_t *block_table;         // [B][max_blocks]
   const int32_t *cache_lens;          // [B]
-  float *workspace;                   // [warps][2][D+2] straddling-pair partials
+  float *workspace;                   // [warps][2][D+4] straddling-pair partials (o, m, l, pad)
   int32_t *tickets;                   // [B][n] merge tickets (zero between launches)
   int32_t layer, num_blocks, n_loc, max_blocks, num_seqs;
   float scale_log2;  // softmax_scale * log2(e)
