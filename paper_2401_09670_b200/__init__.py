@@ -186,10 +186,11 @@ class Pool:
         h = ctypes.c_void_p()
         _check(_lib.ds_pool_create(num_blocks, ctypes.byref(h)))
         self._h = h
+        self._lib = _lib  # kept alive for __del__ at interpreter shutdown
 
     def close(self):
         if getattr(self, "_h", None):
-            _lib.ds_pool_destroy(self._h)
+            self._lib.ds_pool_destroy(self._h)
             self._h = None
 
     __del__ = close
@@ -321,10 +322,11 @@ class Comm:
         buf = ctypes.create_string_buffer(unique_id, 128)
         _check(_lib.ds_comm_init(buf, nranks, rank, ctypes.byref(h)))
         self._h, self.rank, self.nranks = h, rank, nranks
+        self._lib = _lib
 
     def close(self):
         if getattr(self, "_h", None):
-            _lib.ds_comm_destroy(self._h)
+            self._lib.ds_comm_destroy(self._h)
             self._h = None
 
     __del__ = close
@@ -373,6 +375,7 @@ class RemoteKVCache:
         buf = ctypes.create_string_buffer(handle, 64)
         _check(_lib.ds_ipc_open_mem(buf, ctypes.byref(base)))
         self.base = base.value
+        self._lib = _lib
         self.desc = ds_kv_cache(self.base + offset, layers, num_blocks, heads, BLOCK_SIZE, head_dim)
 
     def ref(self):
@@ -380,7 +383,7 @@ class RemoteKVCache:
 
     def close(self):
         if getattr(self, "base", None):
-            _lib.ds_ipc_close_mem(self.base)
+            self._lib.ds_ipc_close_mem(self.base)
             self.base = None
 
     __del__ = close
@@ -399,6 +402,7 @@ class IpcEvent:
             _check(_lib.ds_event_open_ipc(ctypes.create_string_buffer(handle, 64), ctypes.byref(h)))
             self.handle = handle
         self._h = h
+        self._lib = _lib
 
     def record(self, stream=None):
         _check(_lib.ds_event_record(self._h, _stream(stream)))
@@ -408,7 +412,7 @@ class IpcEvent:
 
     def close(self):
         if getattr(self, "_h", None):
-            _lib.ds_event_destroy(self._h)
+            self._lib.ds_event_destroy(self._h)
             self._h = None
 
     __del__ = close
