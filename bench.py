@@ -74,6 +74,8 @@ def parse():
     p.add_argument("--impl", default="ds", choices=["ds", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=6)
+    p.add_argument("--stream-layers", action="store_true",
+                   help="migrate each layer's pages right after its prefill (NEXT-2; LOCAL/NCCL transports)")
     p.add_argument("--e2e-trace", action="store_true", help="print a per-step copy/compute timeline to stderr")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graphs", action="store_true", help="eager decode launches (no CUDA graphs)")
@@ -207,7 +209,7 @@ def _i32(torch, a):
 class Engine:
     """Device state of one rank: pools, resident inputs, staging, CUDA graphs."""
 
-    def __init__(self, w: Workload, role, comm, seed, torch, ds, transport="nccl"):
+    def __init__(self, w: Workload, role, comm, seed, torch, ds, transport="nccl", stream_layers=False):
         self.w, self.role, self.comm, self.torch, self.ds = w, role, comm, torch, ds
         dev = "cuda"
         bf = torch.bfloat16
@@ -256,6 +258,11 @@ class Engine:
             self.graphs = None
         nblk = sum(w.pages)
         self.transport = "local" if role.phase == "both" else transport
+        # NEXT-2: migrate layer l as soon as its prefill is done, so the
+        # transfer overlaps the prefill of the next layers (LOCAL: on a side stream;
+        # NCCL: the library's own side stream). PULL stays whole-batch.
+        self.stream_layers = stream_layers and self.transport in ("local", "nccl")
+        self.mig_stream = torch.cuda.Stream() if (self.stream_layers and self.transport == "local") else None
         self.mrole = {"local": ds.DS_MIGRATE_LOCAL, "pull": ds.DS_MIGRATE_PULL}.get(
             self.transport, ds.DS_MIGRATE_SEND if role.phase == "prefill" else ds.DS_MIGRATE_RECV)
         cache_for_size = self.P if self.pf else self.D
@@ -363,6 +370,7 @@ class Engine:
         tp = np.full((w.B, w.maxb), -1, np.int32)
         ds.ds_block_table(self.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
         tp_d = self.upload(tp)
+        src_ids = self.page_ids(tp_d)
         for layer in range(w.L):
             i = layer % len(self.q)
             if self.layer_hook:
@@ -371,23 +379,37 @@ class Engine:
                                w.scale)
             if self.layer_hook:
                 self.layer_hook("after", layer)
+            if self.stream_layers:
+                self.migrate_layers(peer, src_ids, layer, 1)
         self.launches += w.L
-        src_ids = self.page_ids(tp_d)
         self._mark(marks, "prefill")
-        if self.transport == "local":
-            ds.ds_kv_migrate(None, self.mrole, 0, self.P, 0, w.L, src_ids, 0, w.n, None,
-                             dst_cache=self.D, dst_block_ids=self.dst_ids)
-            self.launches += 1
-        elif self.transport == "nccl":
-            ds.ds_kv_migrate(self.comm, self.mrole, peer, self.P, 0, w.L, src_ids, 0, w.n, self.staging)
-            self.launches += self.migrate_chunks()
-        else:  # pull: publish the batch; the decoder fetches it when it has memory
+        if self.transport == "pull":  # publish the batch; the decoder fetches it when it has memory
             self.pull_publish(peer, tp)
             self._mark(marks, "migrate")
             return
+        if not self.stream_layers:
+            self.migrate_layers(peer, src_ids, 0, w.L)
+        if self.mig_stream is not None:
+            self.torch.cuda.current_stream().wait_stream(self.mig_stream)
         # the pages are free again once the (stream-ordered) migration has read them
         ds.ds_block_table(self.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
         self._mark(marks, "migrate")
+
+    def migrate_layers(self, peer, src_ids, layer_begin, layer_count):
+        """a4-a6 for layers [layer_begin, +layer_count) of this batch towards `peer`"""
+        ds, w, torch = self.ds, self.w, self.torch
+        if self.transport == "local":
+            st = self.mig_stream
+            if st is not None:
+                st.wait_stream(torch.cuda.current_stream())  # the prefill of these layers is done
+            with torch.cuda.stream(st if st is not None else torch.cuda.current_stream()):
+                ds.ds_kv_migrate(None, self.mrole, 0, self.P, layer_begin, layer_count, src_ids, 0, w.n, None,
+                                 dst_cache=self.D, dst_block_ids=self.dst_ids)
+            self.launches += 1
+        else:
+            ds.ds_kv_migrate(self.comm, self.mrole, peer, self.P, layer_begin, layer_count, src_ids, 0, w.n,
+                             self.staging)
+            self.launches += self.migrate_chunks(layer_count)
 
     # -- one-sided pull (CUDA IPC) ----------------------------------------------------
     def pull_setup(self, roles, ctl):
@@ -471,14 +493,17 @@ class Engine:
             self.launches += 1
         else:
             self.admit()
-            ds.ds_kv_migrate(self.comm, self.mrole, role.peer, self.D, 0, w.L, self.dst_ids, 0, w.n, self.staging)
-            self.launches += self.migrate_chunks()
+            # the receiver posts the same per-layer (or whole-batch) calls as its sender
+            per = [(l, 1) for l in range(w.L)] if self.stream_layers else [(0, w.L)]
+            for l0, nl in per:
+                ds.ds_kv_migrate(self.comm, self.mrole, role.peer, self.D, l0, nl, self.dst_ids, 0, w.n, self.staging)
+                self.launches += self.migrate_chunks(nl)
         self._mark(marks, "migrate")
 
-    def migrate_chunks(self):
+    def migrate_chunks(self, layers):
         w = self.w
         chunk_rows = max(1, (64 << 20) // (w.n * 16 * w.d * 2))
-        return -(-(2 * w.L * sum(w.pages)) // chunk_rows)  # pack or unpack kernels (+ NCCL's own)
+        return -(-(2 * layers * sum(w.pages)) // chunk_rows)  # pack or unpack kernels (+ NCCL's own)
 
     def admit(self):
         """decode-side admission of one batch (pull): pages for the prompts"""
@@ -693,7 +718,7 @@ def run_ds(args):
         comm = ds.ds_comm_init(pairing.bootstrap_unique_id(ds.ds_comm_get_unique_id, rank, world, dist), world, rank)
     replicas = 1 if world == 1 else sum(1 for r in roles if r.phase == "decode") // (cfg["tp"] * cfg["pp"])
     eng = Engine(w, role, comm, seed=1234 + role.replica * 7919 + role.stage * 131 + role.tp_rank, torch=torch,
-                 ds=ds, transport=args.transport)
+                 ds=ds, transport=args.transport, stream_layers=args.stream_layers)
     if world > 1 and args.transport == "pull":
         import torch.distributed as dist
         ctl = dist.group.WORLD if args.pg_backend == "gloo" else dist.new_group(backend="gloo")
@@ -752,7 +777,13 @@ def run_ds(args):
         t_roof = w.L * max(w.prefill_flops_per_layer() / (peaks["bf16_tflops"] * 1e12),
                            w.prefill_bytes_per_layer() / (peaks["hbm_gbs"] * 1e9))
         comp["prefill_frac_of_attainable_roofline"] = t_roof / (pf_ms / 1e3)
-    if (role.phase != "decode" or world > 1) and not (args.transport == "pull" and role.phase == "prefill"):
+    if eng.pf and eng.stream_layers:
+        # per-layer migration is issued inside the prefill loop: the prefill segment holds
+        # both, the migrate segment only the tail the last layers' transfer adds
+        comp["migration"] = "streamed per layer (overlaps prefill)"
+        comp["prefill_with_migration_ms_per_batch"] = pf_ms + phase_ms("migrate") / nb
+        comp["migrate_tail_ms_per_batch"] = phase_ms("migrate") / nb
+    elif (role.phase != "decode" or world > 1) and not (args.transport == "pull" and role.phase == "prefill"):
         mig_ms = phase_ms("migrate") / nb  # (a pull prefill rank only publishes; its decoders move the bytes)
         comp["migrate_ms_per_batch"] = mig_ms
         comp["kv_migrate_GBps"] = w.kv_payload_bytes() / (mig_ms / 1e3) / 1e9

@@ -302,6 +302,61 @@ def test_migrate_local_bit_exact(oracle_mod):
         assert pages_match(bits, dst.opool, layer, lens, td)
 
 
+@pytest.mark.parametrize("mode", ["self", "local_side_stream"])
+def test_migrate_streamed_per_layer(oracle_mod, mode):
+    """NEXT-2: layer l is migrated right after its prefill, while
+    the next layers are still being computed (SELF: NCCL on the library's side
+    stream; LOCAL: the copy kernel on a torch side stream). Every layer gets its
+    own inputs, so a transfer that ran ahead of its prefill, or picked up the
+    wrong layer, shows up as a page mismatch."""
+    lens = [300, 17, 64]
+    n, d, L = 8, 128, 5
+    B = len(lens)
+    src = Side(oracle_mod, L, 40, n, d)
+    dst = Side(oracle_mod, L, 50, n, d)
+    dst.fragment(6, 8)
+    tp, tpo = np.full((B, 20), -1, np.int32), np.full((B, 20), -1, np.int32)
+    td, tdo = tp.copy(), tpo.copy()
+    src.append([0] * B, lens, tp, tpo)
+    dst.append([0] * B, lens, td, tdo)
+    sblk = np.concatenate([tp[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+    dblk = np.concatenate([td[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+    sblk_d, dblk_d, tp_d = i32(sblk), i32(dblk), i32(tp)
+    batches = [syn.prefill_batch(40 + layer, lens, n, d) for layer in range(L)]
+    dev_in = [(to_dev(b.q), to_dev(b.k), to_dev(b.v)) for b in batches]
+    cu = i32(batches[0].cu_seqlens)
+    out = torch.empty((sum(lens), n, d), dtype=torch.bfloat16, device="cuda")
+    comm = staging = side = None
+    if mode == "self":
+        comm = ds.ds_comm_init(ds.ds_comm_get_unique_id(), 1, 0)
+        staging = torch.empty(ds.ds_kv_migrate_staging_bytes(src.cache, ds.DS_MIGRATE_SELF, 1, len(sblk), n),
+                              dtype=torch.uint8, device="cuda")
+    else:
+        side = torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    for layer in range(L):
+        q, k, v = dev_in[layer]
+        ds.ds_prefill_attn(q, k, v, out, cu, max(lens), src.cache, layer, tp_d, 0.088)
+        if mode == "self":
+            ds.ds_kv_migrate(comm, ds.DS_MIGRATE_SELF, 0, src.cache, layer, 1, sblk_d, 0, n, staging,
+                             dst_cache=dst.cache, dst_block_ids=dblk_d)
+        else:
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                ds.ds_kv_migrate(None, ds.DS_MIGRATE_LOCAL, 0, src.cache, layer, 1, sblk_d, 0, n, None,
+                                 dst_cache=dst.cache, dst_block_ids=dblk_d)
+        src.opool.write_prefill(layer, batches[layer].k, batches[layer].v, batches[layer].cu_seqlens, tpo)
+    if side is not None:
+        main.wait_stream(side)
+    torch.cuda.synchronize()
+    if comm is not None:
+        comm.close()
+    oracle_mod.migrate(src.opool, dst.opool, 0, L, sblk, dblk, 0, 0, n)
+    bits = to_bits(dst.cache.tensor)
+    for layer in range(L):
+        assert pages_match(bits, dst.opool, layer, lens, td)
+
+
 def test_end_to_end_prefill_migrate_decode(oracle_mod):
     """The whole path for one small batch: prefill -> migrate (SELF) -> 3 decode
     steps on the decode pool, compared with the oracle doing the same."""
