@@ -234,6 +234,38 @@ DS_DEVICE void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
 DS_DEVICE void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 DS_DEVICE void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// ----------------------------------------------------------------- cluster launch control
+// Work stealing without atomics (sm_100): ask the hardware to cancel the launch of
+// a CTA that has not started yet; the 16-B response lands in smem and completes
+// 16 tx-bytes on `bar`. If it succeeded, the caller does that CTA's work.
+DS_DEVICE void clc_try_cancel(uint32_t resp_smem, uint64_t *bar) {
+  asm volatile("clusterlaunchcontrol.try_cancel.async.shared::cta.mbarrier::complete_tx::bytes.b128 [%0], [%1];"
+               ::"r"(resp_smem), "r"(smem_u32(bar))
+               : "memory");
+}
+// decode a response: true (and the cancelled CTA's blockIdx) if a launch was taken over
+DS_DEVICE bool clc_query(const void *resp, int &x, int &y, int &z) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(resp))
+               : "memory");
+  uint32_t ok, cx = 0, cy = 0, cz = 0;
+  asm volatile(
+      "{\n\t.reg .b128 R;\n\t.reg .pred P;\n\t"
+      "mov.b128 R, {%4, %5};\n\t"
+      "clusterlaunchcontrol.query_cancel.is_canceled.pred.b128 P, R;\n\t"
+      "selp.u32 %0, 1, 0, P;\n\t"
+      "@P clusterlaunchcontrol.query_cancel.get_first_ctaid.v4.b32.b128 {%1, %2, %3, _}, R;\n\t}"
+      : "=r"(ok), "+r"(cx), "+r"(cy), "+r"(cz)
+      : "l"((uint64_t)r.x | ((uint64_t)r.y << 32)), "l"((uint64_t)r.z | ((uint64_t)r.w << 32))
+      : "memory");
+  x = (int)cx;
+  y = (int)cy;
+  z = (int)cz;
+  return ok != 0;
+}
+
 // ----------------------------------------------------------------- UMMA descriptors
 // Shared-memory matrix descriptor (sm100, "version 1"), SWIZZLE_128B:
 //   [0,14)  start address >> 4

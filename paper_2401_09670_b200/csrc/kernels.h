@@ -58,11 +58,13 @@ struct PrefillArgs {
   int32_t num_seqs, n_loc, max_blocks, num_q_tiles;
   int32_t layer, num_blocks;   // cache layer / pool pages
   float scale_log2;
+  int32_t persistent;          // CTAs take over unlaunched CTAs' items (cluster launch control)
 };
 cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
                            const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
                            cudaStream_t stream);
 size_t prefill_smem_bytes(int head_dim);
+bool prefill_persistent(int max_len);  // run the prefill CTAs persistently for this length?
 // experimental (DS_PREFILL_KERNEL=2q): two 128-row q tiles per CTA, 128-key tiles
 cudaError_t launch_prefill2q(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
                              const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim, cudaStream_t stream);

@@ -6,7 +6,10 @@
 //   out[i] = sum_{j<=i} softmax_j(scale * q[i].k[j]) v[j]     per (sequence, head)
 //   cache[layer][K|V][bt[r][t/16]][h][t%16] = k|v[t][h]       (a3)
 //
-// B200 design — one CTA per (128-row q tile, head, sequence), TWO CTAs per SM:
+// B200 design — one grid CTA per (128-row q tile, head, sequence), TWO CTAs per
+// SM, run persistently: a CTA that finishes an item takes over the next CTA that
+// has not launched yet (cluster launch control), so each SM slot streams items
+// back to back with the next item's loads overlapping this item's tail:
 //   * kv tiles of 64 keys: smem holds Q (32 KiB) + 2 K stages + 2 V stages
 //     (4 x 16 KiB, 128B-swizzled, TMA-fed) = 96 KiB at head_dim 128; TMEM holds
 //     256 columns = S0 | S1 (64 fp32 columns each, double-buffered) | O (128).
@@ -26,6 +29,8 @@
 //             rounded to bf16 and written back over its S buffer in TMEM
 //             (tcgen05.st), lazy warp-uniform O rescale in TMEM, final
 //             O / l -> bf16 -> global.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -47,16 +52,41 @@ struct Smem {
   static constexpr uint32_t Q = 0;
   static constexpr uint32_t K0 = Q + kQTile;           // 2 stages
   static constexpr uint32_t V0 = K0 + 2 * kKVTile;     // 2 stages
-  static constexpr uint32_t BAR = V0 + 2 * kKVTile;
-  static constexpr uint32_t kBars = 14;
+  static constexpr uint32_t CLC = V0 + 2 * kKVTile;    // 2 x 16-B work-stealing responses
+  static constexpr uint32_t BAR = CLC + 32;
+  static constexpr uint32_t kBars = 21;
   static constexpr uint32_t TMEM_SLOT = BAR + kBars * 8;
   static constexpr uint32_t TOTAL = TMEM_SLOT + 16;
   static constexpr uint32_t ALLOC = TOTAL + 1024;  // slack for 1024-B alignment
 };
 
-// barrier indices ([2] = per stage / per S buffer)
-enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_P = 11, B_O = 12 };
+// barrier indices ([2] = per stage / per S buffer / per response slot)
+enum {
+  B_Q = 0,      // Q tile landed (once per item)
+  B_QE = 1,     // Q no longer read: the item's last S MMA completed
+  B_KF = 2,     // [2] K stage full
+  B_VF = 4,     // [2] V stage full
+  B_KE = 6,     // [2] K stage consumed by S MMA
+  B_VE = 8,     // [2] V stage consumed by P.V MMA
+  B_SF = 10,    // [2] S buffer written by the MMA
+  B_P = 12,     // [2] P written over S buffer (128 softmax threads)
+  B_O = 14,     // [2] O += P_g V_g completed, per S buffer (g & 1)
+  B_OE = 16,    // O read out by the epilogue (128 softmax threads, once per item)
+  B_CLC = 17,   // [2] work-stealing response landed
+  B_CLCE = 19,  // [2] response read by all 6 warps
+};
 
+// Persistent via cluster launch control: the grid keeps one CTA per (q tile, head,
+// sequence) — the hardware's launch order keeps the q tiles of one (sequence, head)
+// together, so their K/V re-reads hit L2 — but a running CTA takes over CTAs that
+// have not launched yet (clusterlaunchcontrol.try_cancel) and runs their items back
+// to back: the producer loads item k+1's Q and K/V while item k's last tiles and
+// epilogue run, so no CTA start-up latency is exposed. All per-tile barrier phases
+// run on a CTA-wide tile counter g (stage = g & 1, phase = (g >> 1) & 1).
+// Measured (tools/kernel_bench.py, vs one item per CTA): 64 x 128 -12 %, 64 x 512
+// -8 %, 16 x 2048 -3 %, 4 x 4096 -5 %, chunked prefill -5..7 %. (The MMA and
+// producer roles must stay under elect.sync: with a plain lane test the compiler
+// loses the uniform datapath for the UMMA operands and every length got slower.)
 template <int D, bool kChunked>
 __global__ void __launch_bounds__(kThreads, 2)
     prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
@@ -64,20 +94,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                    const PrefillArgs a) {
   using S = Smem<D>;
   constexpr int kChunks = D / 64;
-  // q tiles of one (sequence, head) are adjacent in launch order so their K/V
-  // re-reads hit L2; within the group the heaviest (longest causal row) goes first
-  const int h = blockIdx.y, r = blockIdx.z;
-  const int i = a.num_q_tiles - 1 - (int)blockIdx.x;
-  const int seq_start = a.cu_seqlens[r];
-  const int len = a.cu_seqlens[r + 1] - seq_start;
-  if (i * kBM >= len) return;
-  // chunked prefill (NEXT-3): the sequence already holds c0 tokens in the paged
-  // cache; kv tiles [0, npt) are that prefix (read from the pages), tiles
-  // [npt, ntiles) are the chunk's own keys 0 .. 2i+1 (64 keys each; the second
-  // diagonal tile is skipped when it lies wholly past the end of the chunk)
-  const int c0 = kChunked ? a.prefix_lens[r] : 0;
-  const int npt = kChunked ? (c0 + kBN - 1) / kBN : 0;
-  const int ntiles = npt + 2 * i + 1 + (len - i * kBM > kBN ? 1 : 0);
 
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -85,10 +101,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t sbase = smem_u32(smem);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S::BAR);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + S::TMEM_SLOT);
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int b = 0; b < (int)S::kBars; ++b) mbar_init(&bars[b], b == B_P ? 128 : 1);
+    for (int b = 0; b < (int)S::kBars; ++b) {
+      const bool per_thread = b == B_P || b == B_P + 1 || b == B_OE;
+      mbar_init(&bars[b], per_thread ? 128 : (b == B_CLCE || b == B_CLCE + 1) ? kThreads / 32 : 1);
+    }
     fence_barrier_init();
   }
   if (warp == 5) {
@@ -100,237 +119,316 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tO = tmem + 128;
+  if (warp == 4 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_kv);
+    tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_cache);
+  }
 
-  if (warp == 4) {
-    // ------------------------------------------------------------ producer
-    if (elect_one()) {
-      tma_prefetch_desc(&tm_q);
-      tma_prefetch_desc(&tm_kv);
-      tma_prefetch_desc(&tm_v);
-      tma_prefetch_desc(&tm_cache);
-      mbar_arrive_expect_tx(&bars[B_Q], S::kQTile);
+  int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;  // current item
+  uint32_t g0 = 0;  // kv tiles of earlier items (CTA-wide tile counter)
+  uint32_t it = 0;  // non-empty items before the current one
+  bool store_pending = false;  // producer: paged TMA stores may still read a stage
+  for (uint32_t q = 0;; ++q) {
+    if (a.persistent && warp == 4 && lane == 0) {  // ask for the next item now; the answer is needed at the end
+      if (q >= 2) mbar_wait(&bars[B_CLCE + (q & 1)], ((q >> 1) - 1) & 1);
+      fence_proxy_async_smem();  // the generic reads of this slot precede the async write
+      mbar_arrive_expect_tx(&bars[B_CLC + (q & 1)], 16);
+      clc_try_cancel(sbase + S::CLC + (q & 1) * 16, &bars[B_CLC + (q & 1)]);
+    }
+    // item: q tiles of one (sequence, head) adjacent in launch order, heaviest first
+    const int h = by, r = bz;
+    const int i = a.num_q_tiles - 1 - bx;
+    const int seq_start = a.cu_seqlens[r];
+    const int len = a.cu_seqlens[r + 1] - seq_start;
+    if (i * kBM < len) {
+      // chunked prefill (NEXT-3): the sequence already holds c0 tokens in the paged
+      // cache; kv tiles [0, npt) are that prefix (read from the pages), tiles
+      // [npt, ntiles) are the chunk's own keys 0 .. 2i+1 (64 keys each; the second
+      // diagonal tile is skipped when it lies wholly past the end of the chunk)
+      const int c0 = kChunked ? a.prefix_lens[r] : 0;
+      const int npt = kChunked ? (c0 + kBN - 1) / kBN : 0;
+      const int ntiles = npt + 2 * i + 1 + (len - i * kBM > kBN ? 1 : 0);
+      const uint32_t gl = g0 + ntiles - 1;  // last tile of this item
+
+      if (warp == 4) {
+        // ------------------------------------------------------------ producer
+        __syncwarp();  // elect.sync needs the whole warp converged (lane 0 issued the CLC request)
+        if (elect_one()) {
+          if (it > 0) mbar_wait(&bars[B_QE], (it - 1) & 1);  // the previous item's S MMAs are done with Q
+          mbar_arrive_expect_tx(&bars[B_Q], S::kQTile);
 #pragma unroll
-      for (int c = 0; c < kChunks; ++c)
-        tma_load_3d(smem + S::Q + c * kChunkBytes128, &tm_q, &bars[B_Q], c * 64, h, seq_start + i * kBM);
-      const int32_t *btr = a.block_table + (size_t)r * a.max_blocks;
-      for (int j = 0; j < ntiles; ++j) {
-        const int st = j & 1;
-        if (kChunked && j < npt) {
-          // prefix tile: up to 4 pages of 16 cached tokens straight from the pool
-          const int p0 = 4 * j, np = min(4, (c0 + 15) / 16 - p0);
-          const uint32_t bytes = (uint32_t)np * 16 * D * 2;
-#pragma unroll
-          for (int kv = 0; kv < 2; ++kv) {
-            if (j >= 2) mbar_wait(&bars[(kv ? B_VE : B_KE) + st], ((j >> 1) - 1) & 1);
-            uint64_t *full = &bars[(kv ? B_VF : B_KF) + st];
-            mbar_arrive_expect_tx(full, bytes);
-            for (int p = 0; p < np; ++p)
-#pragma unroll
-              for (int c = 0; c < kChunks; ++c)
-                tma_load_4d(smem + (kv ? S::V0 : S::K0) + st * S::kKVTile + c * kChunkBytes64 + p * 16 * 128,
-                            &tm_cache, full, c * 64, 0, h, (a.layer * 2 + kv) * a.num_blocks + btr[p0 + p]);
+          for (int c = 0; c < kChunks; ++c)
+            tma_load_3d(smem + S::Q + c * kChunkBytes128, &tm_q, &bars[B_Q], c * 64, h, seq_start + i * kBM);
+          if (store_pending) {  // the previous item's paged stores read the stages we refill now
+            bulk_wait_group_read0();
+            store_pending = false;
           }
-          continue;
-        }
-        const int kv0 = seq_start + (j - npt) * kBN;
-        if (j >= 2) mbar_wait(&bars[B_KE + st], ((j >> 1) - 1) & 1);  // S_{j-2} has consumed K stage
-        mbar_arrive_expect_tx(&bars[B_KF + st], S::kKVTile);
+          const int32_t *btr = a.block_table + (size_t)r * a.max_blocks;
+          for (int j = 0; j < ntiles; ++j) {
+            const uint32_t g = g0 + j;
+            const int st = g & 1;
+            const uint32_t ph_free = ((g >> 1) - 1) & 1;  // release of tile g-2 from this stage
+            if (kChunked && j < npt) {
+              // prefix tile: up to 4 pages of 16 cached tokens straight from the pool
+              const int p0 = 4 * j, np = min(4, (c0 + 15) / 16 - p0);
+              const uint32_t bytes = (uint32_t)np * 16 * D * 2;
 #pragma unroll
-        for (int c = 0; c < kChunks; ++c)
-          tma_load_3d(smem + S::K0 + st * S::kKVTile + c * kChunkBytes64, &tm_kv, &bars[B_KF + st], c * 64, h, kv0);
-        if (j >= 2) mbar_wait(&bars[B_VE + st], ((j >> 1) - 1) & 1);  // PV_{j-2} has consumed V stage
-        mbar_arrive_expect_tx(&bars[B_VF + st], S::kKVTile);
+              for (int kv = 0; kv < 2; ++kv) {
+                if (g >= 2) mbar_wait(&bars[(kv ? B_VE : B_KE) + st], ph_free);
+                uint64_t *full = &bars[(kv ? B_VF : B_KF) + st];
+                mbar_arrive_expect_tx(full, bytes);
+                for (int p = 0; p < np; ++p)
 #pragma unroll
-        for (int c = 0; c < kChunks; ++c)
-          tma_load_3d(smem + S::V0 + st * S::kKVTile + c * kChunkBytes64, &tm_v, &bars[B_VF + st], c * 64, h, kv0);
-      }
-      // a3: the diagonal K/V tiles 2i (pages 8i..8i+3) and 2i+1 (8i+4..8i+7) -> paged cache
-      // (chunked mode appends the chunk with ds' append kernel instead: the chunk
-      // need not start on a page boundary)
-      const int npg = kChunked ? 0 : min(8, (len - i * kBM + 15) >> 4);
-      const int32_t *bt = btr + i * 8;
-      for (int t = npt + 2 * i; npg > 0 && t < ntiles; ++t) {
-        const int st = t & 1;
-        mbar_wait(&bars[B_KF + st], (t >> 1) & 1);
-        mbar_wait(&bars[B_VF + st], (t >> 1) & 1);
-        for (int p = (t - 2 * i) * 4; p < min(npg, (t - 2 * i) * 4 + 4); ++p) {
-          const int blk = bt[p];
-#pragma unroll
-          for (int kv = 0; kv < 2; ++kv)
+                  for (int c = 0; c < kChunks; ++c)
+                    tma_load_4d(smem + (kv ? S::V0 : S::K0) + st * S::kKVTile + c * kChunkBytes64 + p * 16 * 128,
+                                &tm_cache, full, c * 64, 0, h, (a.layer * 2 + kv) * a.num_blocks + btr[p0 + p]);
+              }
+              continue;
+            }
+            const int kv0 = seq_start + (j - npt) * kBN;
+            if (g >= 2) mbar_wait(&bars[B_KE + st], ph_free);  // S_{g-2} has consumed the K stage
+            mbar_arrive_expect_tx(&bars[B_KF + st], S::kKVTile);
 #pragma unroll
             for (int c = 0; c < kChunks; ++c)
-              tma_store_4d(&tm_cache,
-                           smem + (kv ? S::V0 : S::K0) + st * S::kKVTile + c * kChunkBytes64 + (p & 3) * 16 * 128,
-                           c * 64, 0, h, (a.layer * 2 + kv) * a.num_blocks + blk);
-        }
-      }
-      bulk_commit_group();
-      // observe the last stage releases too (every mbarrier phase is waited on;
-      // also guarantees the final MMAs have drained before the CTA retires)
-      for (int t = max(0, ntiles - 2); t < ntiles; ++t) {
-        mbar_wait(&bars[B_KE + (t & 1)], (t >> 1) & 1);
-        mbar_wait(&bars[B_VE + (t & 1)], (t >> 1) & 1);
-      }
-      bulk_wait_group_read0();
-    }
-    __syncwarp();
-  } else if (warp == 5) {
-    // ------------------------------------------------------------ MMA issuer
-    if (elect_one()) {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
-      constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, D, 0, 1);
-      mbar_wait(&bars[B_Q], 0);
-      auto issue_pv = [&](int jj) {  // O += P_jj V_jj
-        const int st = jj & 1;
-        mbar_wait(&bars[B_P], jj & 1);
-        mbar_wait(&bars[B_VF + st], (jj >> 1) & 1);
-        tc_fence_after();
+              tma_load_3d(smem + S::K0 + st * S::kKVTile + c * kChunkBytes64, &tm_kv, &bars[B_KF + st], c * 64, h,
+                          kv0);
+            if (g >= 2) mbar_wait(&bars[B_VE + st], ph_free);  // PV_{g-2} has consumed the V stage
+            mbar_arrive_expect_tx(&bars[B_VF + st], S::kKVTile);
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)  // 16 keys = 8 packed P columns per step
-          umma_ts(tO, tmem + st * kBN + kk * 8,
-                  smem_desc_sw128(sbase + S::V0 + st * S::kKVTile + kk * 16 * 128, kChunkBytes64, 1024), idesc_o,
-                  (jj > 0 || kk > 0));
-        umma_commit(&bars[B_O]);
-        umma_commit(&bars[B_VE + st]);
-      };
-      for (int j = 0; j < ntiles; ++j) {
-        const int st = j & 1;
-        mbar_wait(&bars[B_KF + st], (j >> 1) & 1);
-        if (j >= 2) mbar_wait(&bars[B_O], (j - 2) & 1);  // P_{j-2} (aliasing S buffer st) consumed
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          umma_ss(tmem + st * kBN, smem_desc_sw128(sbase + S::Q + (kk >> 2) * kChunkBytes128 + (kk & 3) * 32, 16, 1024),
-                  smem_desc_sw128(sbase + S::K0 + st * S::kKVTile + (kk >> 2) * kChunkBytes64 + (kk & 3) * 32, 16,
-                                  1024),
-                  idesc_s, kk > 0);
-        umma_commit(&bars[B_SF + st]);
-        umma_commit(&bars[B_KE + st]);
-        if (j >= 1) issue_pv(j - 1);
-      }
-      // observe O's second-to-last completion before the last commit (the softmax
-      // only waits on O when it rescales; every phase is waited on by someone)
-      if (ntiles >= 2) mbar_wait(&bars[B_O], (ntiles - 2) & 1);
-      issue_pv(ntiles - 1);
-    }
-    __syncwarp();
-  } else {
-    // ------------------------------------------------------------ softmax warps 0-3
-    const int row = threadIdx.x;  // TMEM lane == q row within the tile
-    const int q_pos = i * kBM + row;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    const float sl2 = a.scale_log2;
-    float m = -__int_as_float(0x7f800000), l = 0.f;
-    for (int j = 0; j < ntiles; ++j) {
-      const int st = j & 1;
-      mbar_wait(&bars[B_SF + st], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t sr[2][32];
-      tmem_ld32(tmem + lane_off + st * kBN, sr[0]);
-      tmem_ld32(tmem + lane_off + st * kBN + 32, sr[1]);
-      tmem_wait_ld();
-      // row max on the raw scores (scale > 0 preserves order); only the two
-      // diagonal tiles are masked (key position > query position)
-      float mx = -__int_as_float(0x7f800000);
-      // prefix tiles: keys at or beyond c0 are not cached yet (masked); chunk
-      // tiles: causal within the chunk (key position > query position masked)
-      const bool prefix_tail = kChunked && j == npt - 1 && (c0 % kBN) != 0;
-      if (prefix_tail || j - npt >= 2 * i) {
-        const int lim = prefix_tail ? c0 - 1 - j * kBN : q_pos - (j - npt) * kBN;  // last visible column
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc)
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            if (cc * 32 + e > lim) sr[cc][e] = 0xff800000u;  // -inf
-            mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
+            for (int c = 0; c < kChunks; ++c)
+              tma_load_3d(smem + S::V0 + st * S::kKVTile + c * kChunkBytes64, &tm_v, &bars[B_VF + st], c * 64, h,
+                          kv0);
           }
-      } else {
+          // a3: the diagonal K/V tiles 2i (pages 8i..8i+3) and 2i+1 (8i+4..8i+7) -> paged
+          // cache (chunked mode appends the chunk with ds' append kernel instead: the
+          // chunk need not start on a page boundary)
+          const int npg = kChunked ? 0 : min(8, (len - i * kBM + 15) >> 4);
+          const int32_t *bt = btr + i * 8;
+          for (int t = npt + 2 * i; npg > 0 && t < ntiles; ++t) {
+            const uint32_t g = g0 + t;
+            const int st = g & 1;
+            mbar_wait(&bars[B_KF + st], (g >> 1) & 1);
+            mbar_wait(&bars[B_VF + st], (g >> 1) & 1);
+            for (int p = (t - npt - 2 * i) * 4; p < min(npg, (t - npt - 2 * i) * 4 + 4); ++p) {
+              const int blk = bt[p];
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc)
+              for (int kv = 0; kv < 2; ++kv)
 #pragma unroll
-          for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
-      }
-      // Conditional rescaling: the exponent base m only moves when this tile's
-      // row max exceeds it by more than kRescaleLog2 (p <= 2^8 in between, exact
-      // in fp32/bf16 range); softmax is invariant to the base, so the result is
-      // the same function — most tiles then skip the O rescale AND the wait on
-      // the previous P.V MMA.
-      const float m_tile = mx * sl2;
-      const bool grow = m_tile > m + kRescaleLog2;
-      const float m_new = grow ? m_tile : m;
-      const float alpha = grow ? ex2(m - m_new) : 1.f;
-      // p = 2^(s*scale*log2e - m): one FFMA + one MUFU ex2 per element; P is
-      // rounded to bf16 (the P operand of the P.V MMA), the row sum stays fp32.
-      uint32_t pk[32];
-      const uint64_t sl2x2 = f2_pack(sl2, sl2), negm2 = f2_pack(-m_new, -m_new);
-      uint64_t rs2 = f2_pack(0.f, 0.f);
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc)
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          // exponent arguments two at a time (FFMA2); kPolyEvery-th exponentials on
-          // the FMA pipe, the rest on MUFU; the fp32 row sum two at a time (FADD2)
-          float x0, x1;
-          f2_unpack(f2_fma(f2_pack(__uint_as_float(sr[cc][e]), __uint_as_float(sr[cc][e + 1])), sl2x2, negm2), x0,
-                    x1);
-          const float p0 = (e % kPolyEvery) == 0 ? ex2_poly(x0) : ex2(x0);
-          const float p1 = ((e + 1) % kPolyEvery) == 0 ? ex2_poly(x1) : ex2(x1);
-          rs2 = f2_add(rs2, f2_pack(p0, p1));
-          pk[cc * 16 + e / 2] = pack_bf16(p0, p1);
+                for (int c = 0; c < kChunks; ++c)
+                  tma_store_4d(&tm_cache,
+                               smem + (kv ? S::V0 : S::K0) + st * S::kKVTile + c * kChunkBytes64 + (p & 3) * 16 * 128,
+                               c * 64, 0, h, (a.layer * 2 + kv) * a.num_blocks + blk);
+            }
+          }
+          if (npg > 0) {
+            bulk_commit_group();
+            store_pending = true;
+          }
         }
-      float rs0, rs1;
-      f2_unpack(rs2, rs0, rs1);
-      l = l * alpha + (rs0 + rs1);
-      m = m_new;
-      if (j > 0 && __any_sync(0xffffffffu, grow)) {  // warp-uniform O rescale, only when a base moved
-        mbar_wait(&bars[B_O], (j - 1) & 1);          // O is not in use by P_{j-1} V_{j-1} any more
+        __syncwarp();
+      } else if (warp == 5) {
+        // ------------------------------------------------------------ MMA issuer
+        // Order per tile g: S_g = Q K_g^T, then O += P_{g-1} V_{g-1} (within an item).
+        // P.V completions are tracked per S buffer (B_O[g & 1]). mbarrier parity waits
+        // are exact only if the waiter has seen the previous phase of that barrier and
+        // the next one cannot have completed yet: this thread waits on P_k V_k for
+        // every k in order (k = g-2 before S_g, or at the end of the previous item)
+        // and always before issuing P_{k+2} V_{k+2}.
+        __syncwarp();
+        if (elect_one()) {
+          constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
+          constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, D, 0, 1);
+          mbar_wait(&bars[B_Q], it & 1);
+          auto issue_pv = [&](uint32_t g, bool first) {  // O (+)= P_g V_g
+            const int st = g & 1;
+            mbar_wait(&bars[B_P + st], (g >> 1) & 1);
+            mbar_wait(&bars[B_VF + st], (g >> 1) & 1);
+            if (first && it > 0) mbar_wait(&bars[B_OE], (it - 1) & 1);  // previous item's O read out
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < kBN / 16; ++kk)  // 16 keys = 8 packed P columns per step
+              umma_ts(tO, tmem + st * kBN + kk * 8,
+                      smem_desc_sw128(sbase + S::V0 + st * S::kKVTile + kk * 16 * 128, kChunkBytes64, 1024),
+                      idesc_o, (!first || kk > 0));
+            umma_commit(&bars[B_O + st]);
+            umma_commit(&bars[B_VE + st]);
+          };
+          for (int j = 0; j < ntiles; ++j) {
+            const uint32_t g = g0 + j;
+            const int st = g & 1;
+            mbar_wait(&bars[B_KF + st], (g >> 1) & 1);
+            // S buffer st still holds P_{g-2}: wait for P_{g-2} V_{g-2} (for j == 0 that
+            // wait already happened at the end of the previous item)
+            if (j >= 1 && g >= 2) mbar_wait(&bars[B_O + st], ((g >> 1) - 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < D / 16; ++kk)
+              umma_ss(tmem + st * kBN,
+                      smem_desc_sw128(sbase + S::Q + (kk >> 2) * kChunkBytes128 + (kk & 3) * 32, 16, 1024),
+                      smem_desc_sw128(sbase + S::K0 + st * S::kKVTile + (kk >> 2) * kChunkBytes64 + (kk & 3) * 32,
+                                      16, 1024),
+                      idesc_s, kk > 0);
+            umma_commit(&bars[B_SF + st]);
+            umma_commit(&bars[B_KE + st]);
+            if (j == ntiles - 1) umma_commit(&bars[B_QE]);
+            if (j >= 1) issue_pv(g - 1, j == 1);
+          }
+          if (gl >= 1) mbar_wait(&bars[B_O + ((gl - 1) & 1)], ((gl - 1) >> 1) & 1);  // frees S buffer gl+1
+          issue_pv(gl, ntiles == 1);
+        }
+        __syncwarp();
+      } else {
+        // ------------------------------------------------------------ softmax warps 0-3
+        const int row = threadIdx.x;  // TMEM lane == q row within the tile
+        const int q_pos = i * kBM + row;
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        const float sl2 = a.scale_log2;
+        float m = -__int_as_float(0x7f800000), l = 0.f;
+        // P_k V_k complete (B_O[k & 1]). Parity waits are exact only if this thread
+        // has seen the previous phase of that barrier and the next cannot complete yet:
+        // it waits on P_{g-2} V_{g-2} at every tile g before publishing P_g (so every
+        // phase of both barriers in order, one tile of slack), and on P_{g-1} V_{g-1}
+        // only to rescale O, and on the last P.V in the epilogue.
+        auto wait_pv = [&](uint32_t k) { mbar_wait(&bars[B_O + (k & 1)], (k >> 1) & 1); };
+        for (int j = 0; j < ntiles; ++j) {
+          const uint32_t g = g0 + j;
+          const int st = g & 1;
+          mbar_wait(&bars[B_SF + st], (g >> 1) & 1);
+          tc_fence_after();
+          uint32_t sr[2][32];
+          tmem_ld32(tmem + lane_off + st * kBN, sr[0]);
+          tmem_ld32(tmem + lane_off + st * kBN + 32, sr[1]);
+          tmem_wait_ld();
+          // row max on the raw scores (scale > 0 preserves order); prefix tiles: keys at
+          // or beyond c0 are not cached yet (masked); chunk tiles: causal within the
+          // chunk (key position > query position masked) — only the diagonal tiles
+          float mx = -__int_as_float(0x7f800000);
+          const bool prefix_tail = kChunked && j == npt - 1 && (c0 % kBN) != 0;
+          if (prefix_tail || j - npt >= 2 * i) {
+            const int lim = prefix_tail ? c0 - 1 - j * kBN : q_pos - (j - npt) * kBN;  // last visible column
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                if (cc * 32 + e > lim) sr[cc][e] = 0xff800000u;  // -inf
+                mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
+              }
+          } else {
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+              for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
+          }
+          // Conditional rescaling: the exponent base m only moves when this tile's row
+          // max exceeds it by more than kRescaleLog2 (p <= 2^8 in between, exact in
+          // fp32/bf16 range); softmax is invariant to the base, so the result is the
+          // same function — most tiles then skip the O rescale AND the wait on the
+          // previous P.V MMA.
+          const float m_tile = mx * sl2;
+          const bool grow = m_tile > m + kRescaleLog2;
+          const float m_new = grow ? m_tile : m;
+          const float alpha = grow ? ex2(m - m_new) : 1.f;
+          // p = 2^(s*scale*log2e - m): one FFMA + one MUFU ex2 per element; P is rounded
+          // to bf16 (the P operand of the P.V MMA), the row sum stays fp32.
+          uint32_t pk[32];
+          const uint64_t sl2x2 = f2_pack(sl2, sl2), negm2 = f2_pack(-m_new, -m_new);
+          uint64_t rs2 = f2_pack(0.f, 0.f);
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              // exponent arguments two at a time (FFMA2); kPolyEvery-th exponentials on
+              // the FMA pipe, the rest on MUFU; the fp32 row sum two at a time (FADD2)
+              float x0, x1;
+              f2_unpack(f2_fma(f2_pack(__uint_as_float(sr[cc][e]), __uint_as_float(sr[cc][e + 1])), sl2x2, negm2),
+                        x0, x1);
+              const float p0 = (e % kPolyEvery) == 0 ? ex2_poly(x0) : ex2(x0);
+              const float p1 = ((e + 1) % kPolyEvery) == 0 ? ex2_poly(x1) : ex2(x1);
+              rs2 = f2_add(rs2, f2_pack(p0, p1));
+              pk[cc * 16 + e / 2] = pack_bf16(p0, p1);
+            }
+          float rs0, rs1;
+          f2_unpack(rs2, rs0, rs1);
+          l = l * alpha + (rs0 + rs1);
+          m = m_new;
+          if (j > 0 && __any_sync(0xffffffffu, grow)) {  // warp-uniform O rescale, only when a base moved
+            wait_pv(g - 1);                              // O is not in use by P_{g-1} V_{g-1} any more
+            tc_fence_after();
+#pragma unroll
+            for (int cc = 0; cc < D / 32; ++cc) {
+              uint32_t o[32];
+              tmem_ld32(tO + lane_off + cc * 32, o);
+              tmem_wait_ld();
+              const uint64_t a2 = f2_pack(alpha, alpha), z2 = f2_pack(0.f, 0.f);
+#pragma unroll
+              for (int e = 0; e < 32; e += 2) {
+                float lo, hi;
+                f2_unpack(f2_fma(f2_pack(__uint_as_float(o[e]), __uint_as_float(o[e + 1])), a2, z2), lo, hi);
+                o[e] = __float_as_uint(lo);
+                o[e + 1] = __float_as_uint(hi);
+              }
+              tmem_st32(tO + lane_off + cc * 32, o);
+            }
+          }
+          if (g >= 2) wait_pv(g - 2);  // keep the observed phases contiguous (normally long complete)
+          // P (bf16 pairs, low half = even key) over the first 32 columns of S buffer st
+          tmem_st32(tmem + lane_off + st * kBN, pk);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive(&bars[B_P + st]);
+        }
+        // epilogue: O / l -> bf16 -> global (rows inside the sequence only)
+        wait_pv(gl);
         tc_fence_after();
+        const float inv_l = 1.f / l;
+        uint16_t *orow = reinterpret_cast<uint16_t *>(a.out) + ((size_t)(seq_start + q_pos) * a.n_loc + h) * D;
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) {
           uint32_t o[32];
           tmem_ld32(tO + lane_off + cc * 32, o);
           tmem_wait_ld();
-          const uint64_t a2 = f2_pack(alpha, alpha), z2 = f2_pack(0.f, 0.f);
+          if (q_pos < len) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            float lo, hi;
-            f2_unpack(f2_fma(f2_pack(__uint_as_float(o[e]), __uint_as_float(o[e + 1])), a2, z2), lo, hi);
-            o[e] = __float_as_uint(lo);
-            o[e + 1] = __float_as_uint(hi);
+            for (int u = 0; u < 4; ++u) {
+              uint4 v;
+              v.x = pack_bf16(__uint_as_float(o[u * 8 + 0]) * inv_l, __uint_as_float(o[u * 8 + 1]) * inv_l);
+              v.y = pack_bf16(__uint_as_float(o[u * 8 + 2]) * inv_l, __uint_as_float(o[u * 8 + 3]) * inv_l);
+              v.z = pack_bf16(__uint_as_float(o[u * 8 + 4]) * inv_l, __uint_as_float(o[u * 8 + 5]) * inv_l);
+              v.w = pack_bf16(__uint_as_float(o[u * 8 + 6]) * inv_l, __uint_as_float(o[u * 8 + 7]) * inv_l);
+              *reinterpret_cast<uint4 *>(orow + cc * 32 + u * 8) = v;
+            }
           }
-          tmem_st32(tO + lane_off + cc * 32, o);
         }
+        tc_fence_before();
+        mbar_arrive(&bars[B_OE]);  // the next item's first P.V may overwrite O
       }
-      // P (bf16 pairs, low half = even key) over the first 32 columns of S buffer st
-      tmem_st32(tmem + lane_off + st * kBN, pk);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&bars[B_P]);
+      g0 += ntiles;
+      ++it;
     }
-    // epilogue: O / l -> bf16 -> global (rows inside the sequence only)
-    mbar_wait(&bars[B_O], (ntiles - 1) & 1);
-    tc_fence_after();
-    const float inv_l = 1.f / l;
-    uint16_t *orow = reinterpret_cast<uint16_t *>(a.out) + ((size_t)(seq_start + q_pos) * a.n_loc + h) * D;
-#pragma unroll
-    for (int cc = 0; cc < D / 32; ++cc) {
-      uint32_t o[32];
-      tmem_ld32(tO + lane_off + cc * 32, o);
-      tmem_wait_ld();
-      if (q_pos < len) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          uint4 v;
-          v.x = pack_bf16(__uint_as_float(o[u * 8 + 0]) * inv_l, __uint_as_float(o[u * 8 + 1]) * inv_l);
-          v.y = pack_bf16(__uint_as_float(o[u * 8 + 2]) * inv_l, __uint_as_float(o[u * 8 + 3]) * inv_l);
-          v.z = pack_bf16(__uint_as_float(o[u * 8 + 4]) * inv_l, __uint_as_float(o[u * 8 + 5]) * inv_l);
-          v.w = pack_bf16(__uint_as_float(o[u * 8 + 6]) * inv_l, __uint_as_float(o[u * 8 + 7]) * inv_l);
-          *reinterpret_cast<uint4 *>(orow + cc * 32 + u * 8) = v;
-        }
-      }
-    }
+    if (!a.persistent) break;
+    // next item: the work-stealing response (every warp reads it, then releases the slot)
+    mbar_wait(&bars[B_CLC + (q & 1)], (q >> 1) & 1);
+    int nx, ny, nz;
+    const bool more = clc_query(smem + S::CLC + (q & 1) * 16, nx, ny, nz);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars[B_CLCE + (q & 1)]);
+    if (!more) break;
+    bx = nx;
+    by = ny;
+    bz = nz;
   }
 
+  if (warp == 4 && lane == 0 && g0 > 0) {
+    // observe the last stage releases too (every mbarrier phase is waited on; also
+    // guarantees the final MMAs have drained before the CTA retires)
+    for (uint32_t t = g0 >= 2 ? g0 - 2 : 0; t < g0; ++t) {
+      mbar_wait(&bars[B_KE + (t & 1)], (t >> 1) & 1);
+      mbar_wait(&bars[B_VE + (t & 1)], (t >> 1) & 1);
+    }
+    bulk_wait_group_read0();
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 5) {
@@ -357,6 +455,16 @@ static cudaError_t launch_one(const PrefillArgs &a, const CUtensorMap &tq, const
 }
 
 }  // namespace
+
+bool prefill_persistent(int /*max_len*/) {
+  // always (faster at every measured length); DS_PREFILL_PERSISTENT=0 runs one
+  // item per CTA for A/B measurements and the parity test of that mode
+  static const bool on = [] {
+    const char *e = getenv("DS_PREFILL_PERSISTENT");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on;
+}
 
 size_t prefill_smem_bytes(int head_dim) {
   return head_dim == 128 ? Smem<128>::ALLOC : Smem<64>::ALLOC;

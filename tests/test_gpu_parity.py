@@ -109,6 +109,29 @@ def test_prefill_many_heads_ragged(oracle_mod):
     assert err <= TOL and err <= WARN_PREFILL, err
 
 
+def test_prefill_work_stealing_stress(oracle_mod):
+    """More CTAs than SM slots, many empty and 1- or 2-tile items: most items run
+    on CTAs that took them over (cluster launch control), back to back. The
+    output must match the oracle and be bit-identical over repeated launches (a
+    cross-item race shows up as run-to-run differences)."""
+    lens = [130, 45, 260, 1, 17, 129, 64, 300]
+    b, side, table, got, err = run_prefill(oracle_mod, lens, 40, 128, seed=12)
+    assert err <= TOL and err <= WARN_PREFILL, err
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, lens, table)
+    q, k, v = to_dev(b.q), to_dev(b.k), to_dev(b.v)
+    out = torch.empty_like(q)
+    first = None
+    for _ in range(10):
+        ds.ds_prefill_attn(q, k, v, out, i32(b.cu_seqlens), max(lens), side.cache, 0, i32(table), 1 / math.sqrt(128))
+        torch.cuda.synchronize()
+        bits = to_bits(out)
+        if first is None:
+            first = bits
+            assert np.array_equal(bits, to_bits(torch.from_numpy(got).to(torch.bfloat16)))
+        else:
+            assert np.array_equal(bits, first)
+
+
 def test_prefill_full_size_config2_sampled(oracle_mod):
     # OPT-13B geometry, 16 x 512-token prompts (8192 tokens): the bench's launch
     g = syn.rng(3)
@@ -561,4 +584,23 @@ def test_experimental_pair_kernel_parity():
                         os.path.join(here, "test_gpu_parity.py"), "-k",
                         "prefill and not chunked and not experimental"], env=env, capture_output=True, text=True,
                        timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("force", ["0", "1"])
+def test_prefill_persistence_forced(force):
+    """The prefill kernel runs persistently (cluster-launch-control work stealing)
+    for short prompts and one item per CTA for long ones; DS_PREFILL_PERSISTENT
+    forces either mode for every length (read once per process), so each mode is
+    checked on every prefill and chunked-prefill parity case, long and ragged ones
+    included."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DS_PREFILL_PERSISTENT=force)
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_parity.py"), "-k",
+                        "(prefill or chunked or streamed or end_to_end) and not experimental and not forced"],
+                       env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
