@@ -53,6 +53,7 @@ def _compile(src, inc, verbose):
            "-I", os.path.join(ROOT, "include"), "-I", inc, "-c", src, "-o", obj + ".tmp"]
     if src.endswith(".cu"):
         cmd += ["-Xptxas", "-v"] if verbose else []
+    cmd += os.environ.get("DS_NVCC_DEFS", "").split()  # A/B variants (tools/ab.sh); empty for the product
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")

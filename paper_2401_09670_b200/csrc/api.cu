@@ -171,6 +171,7 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
   a.max_blocks = max_blocks_per_seq;
   a.num_q_tiles = two_q ? (max_seqlen + 255) / 256 : (max_seqlen + 127) / 128;
   a.persistent = prefill_persistent(max_seqlen);
+  a.band_groups = prefill_band_groups(max_seqlen, D);
   a.layer = layer;
   a.num_blocks = cache->num_blocks;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
@@ -218,6 +219,7 @@ extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const
   a.max_blocks = max_blocks_per_seq;
   a.num_q_tiles = (max_chunk_len + 127) / 128;
   a.persistent = prefill_persistent(max_context_len);  // an item attends the prefix + its chunk rows
+  a.band_groups = prefill_band_groups(max_context_len, D);
   a.layer = layer;
   a.num_blocks = cache->num_blocks;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;

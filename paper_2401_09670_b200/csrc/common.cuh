@@ -108,6 +108,22 @@ DS_DEVICE void mbar_wait(uint64_t *bar, uint32_t parity) {
   }
 }
 
+// the same with a suspend-time hint: the waiting thread may sleep (no issue slots)
+// until the phase completes or `ns` nanoseconds pass — for producer / MMA threads
+// that spend most of their time waiting next to latency-bound compute warps
+DS_DEVICE void mbar_wait_sleep(uint64_t *bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+        : "memory");
+  } while (!ok);
+}
+
 // make generic-proxy smem writes visible to the async proxy (TMA / UMMA)
 DS_DEVICE void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -154,6 +170,13 @@ DS_DEVICE void bulk_g2s(void *smem_dst, const void *gsrc, uint32_t bytes, uint64
           smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// bring [gsrc, gsrc + bytes) into L2 without a destination (size multiple of 16):
+// keeps DRAM requests in flight beyond what the shared-memory ring can hold
+DS_DEVICE void bulk_prefetch_l2(const void *gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes)
+               : "memory");
 }
 
 // ----------------------------------------------------------------- tcgen05 / TMEM

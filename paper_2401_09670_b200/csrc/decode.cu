@@ -49,18 +49,31 @@ struct DecCfg {
   static constexpr int kSmem = kBarOff + kWarps * kSlots * 8;
 };
 
-DS_DEVICE float dot8(const float (&q)[8], const uint4 &k) {
-  float s = q[0] * bf16lo(k.x);
-  s = fmaf(q[1], bf16hi(k.x), s);
-  s = fmaf(q[2], bf16lo(k.y), s);
-  s = fmaf(q[3], bf16hi(k.y), s);
-  s = fmaf(q[4], bf16lo(k.z), s);
-  s = fmaf(q[5], bf16hi(k.z), s);
-  s = fmaf(q[6], bf16lo(k.w), s);
-  s = fmaf(q[7], bf16hi(k.w), s);
-  return s;
+// f32 = bf16 * bf16 + f32 in one instruction (sm_100 FHFMA.BF16, operands read
+// straight from either half of a packed register; the bf16 x bf16 product is exact)
+DS_DEVICE float fma_bf16(uint16_t a, uint16_t b, float c) {
+  float d;
+  asm("fma.rn.f32.bf16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+  return d;
+}
+DS_DEVICE void halves(uint32_t x, uint16_t &lo, uint16_t &hi) {
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(x));
 }
 
+// q.k over 8 dims, bf16 q and k, fp32 accumulation in two chains
+DS_DEVICE float dot8(const uint4 &q, const uint4 &k) {
+  uint16_t q0, q1, q2, q3, q4, q5, q6, q7, k0, k1, k2, k3, k4, k5, k6, k7;
+  halves(q.x, q0, q1); halves(q.y, q2, q3); halves(q.z, q4, q5); halves(q.w, q6, q7);
+  halves(k.x, k0, k1); halves(k.y, k2, k3); halves(k.z, k4, k5); halves(k.w, k6, k7);
+  float s = fma_bf16(q0, k0, 0.f), t = fma_bf16(q1, k1, 0.f);
+  s = fma_bf16(q2, k2, s); t = fma_bf16(q3, k3, t);
+  s = fma_bf16(q4, k4, s); t = fma_bf16(q5, k5, t);
+  s = fma_bf16(q6, k6, s); t = fma_bf16(q7, k7, t);
+  return s + t;
+}
+
+// acc += p * v over 8 dims (fp32 weight: rounding p to bf16 for FHFMA measured
+// no faster and costs accuracy)
 DS_DEVICE void axpy8(float (&acc)[8], float p, const uint4 &v) {
   acc[0] = fmaf(p, bf16lo(v.x), acc[0]);
   acc[1] = fmaf(p, bf16hi(v.x), acc[1]);
@@ -240,9 +253,9 @@ DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int 
 // dims [8*dpart, 8*dpart+8). kLast: the page holding position c (masked; token c
 // comes from k_new/v_new).
 template <int D, bool kLast>
-DS_DEVICE void consume_page(const uint8_t *kst, const uint8_t *vst, const float (&q)[8], float (&acc)[8],
-                            float &m, float &l, int lane, int pos0, int c, const uint16_t *knew,
-                            const uint16_t *vnew) {
+DS_DEVICE void consume_page(const uint8_t *kst, const uint8_t *vst, const uint4 &q, float (&acc)[8],
+                            float &m, float &l, int lane, int pos0, int c, float scale_log2,
+                            const uint16_t *knew, const uint16_t *vnew) {
   constexpr int TPG = D / 8, GPW = 32 / TPG, NIT = 16 / GPW;  // NIT == TPG / 2
   const int g = lane / TPG, dpart = lane % TPG;
   // q.k partial sums of this lane's NIT rows
@@ -270,7 +283,7 @@ DS_DEVICE void consume_page(const uint8_t *kst, const uint8_t *vst, const float 
     }
     cnt >>= 1;
   }
-  float s = v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+  float s = (v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1)) * scale_log2;
   const int my_t = ((lane >> 1) & (NIT - 1)) * GPW + g;
   if (kLast && pos0 + my_t > c) s = kNegInf;
   // warp max / sum over the 16 distinct scores (skip xor 1: duplicates)
@@ -339,17 +352,31 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   const size_t kv_stride = (size_t)a.num_blocks * n * page_elems;  // K -> V
   const uint16_t *layer_base = a.cache + (size_t)a.layer * 2 * kv_stride;
 
-  // producer (lane 0): TMA bulk copies of K/V pages, kSlots half-pages ahead
-  PagePos pq = locate(x0, prefix, B, n);
+  // producer (lane 0): a page cursor that reads the block table one page ahead
+  // (the load is consumed a step later, so lane 0 — and with it the consuming
+  // warp — does not stall on it); the TMA bulk copies of K/V pages run kSlots
+  // half-pages ahead of the consumer. (An L2 prefetch of pages further ahead —
+  // cp.async.bulk.prefetch or per-lane prefetch.global.L2 — was measured 10-40 %
+  // SLOWER at every batch size and is not used.)
+  PagePos pf = locate(x0, prefix, B, n);
+  int blk_next = 0;
+  if (lane == 0) blk_next = a.block_table[(size_t)pf.b * a.max_blocks + pf.p];
+  int64_t x_pf = x0;
+  auto next_page = [&]() {  // pool offset (in pages) of page x_pf; advances the cursor
+    const size_t off = (size_t)blk_next * n + pf.h;
+    if (++x_pf < x1) {
+      advance(pf, prefix, n);
+      blk_next = a.block_table[(size_t)pf.b * a.max_blocks + pf.p];
+    }
+    return off;
+  };
   const int64_t h_end = 2 * (x1 - x0);  // half-pages of this warp
   int64_t h_issued = 0;
   const uint16_t *cur_page = nullptr;
   auto issue = [&]() {
     const int slot = (int)(h_issued % C::kSlots);
     if ((h_issued & 1) == 0) {
-      const int blk = a.block_table[(size_t)pq.b * a.max_blocks + pq.p];
-      cur_page = layer_base + ((size_t)blk * n + pq.h) * page_elems;
-      advance(pq, prefix, n);
+      cur_page = layer_base + next_page() * page_elems;
     }
     mbar_arrive_expect_tx(&wbar[slot], C::kPageBytes);
     bulk_g2s(ring + slot * C::kPageBytes, cur_page + ((h_issued & 1) ? kv_stride : 0), C::kPageBytes,
@@ -363,17 +390,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   PagePos cq = locate(x0, prefix, B, n);
   int seg_begin = cq.p;  // the first segment may start mid-pair
   bool first_seg = true;
-  float q[8], m = kNegInf, l = 0.f, acc[8];
+  uint4 qv;
+  float m = kNegInf, l = 0.f, acc[8];
   int c = 0;
   size_t row = 0;
   auto load_pair = [&]() {
     row = ((size_t)cq.b * n + cq.h) * D + dpart * 8;
-    const uint4 qv = *reinterpret_cast<const uint4 *>(a.q + row);
-    const float s = a.scale_log2;
-    q[0] = bf16lo(qv.x) * s; q[1] = bf16hi(qv.x) * s;
-    q[2] = bf16lo(qv.y) * s; q[3] = bf16hi(qv.y) * s;
-    q[4] = bf16lo(qv.z) * s; q[5] = bf16hi(qv.z) * s;
-    q[6] = bf16lo(qv.w) * s; q[7] = bf16hi(qv.w) * s;
+    qv = *reinterpret_cast<const uint4 *>(a.q + row);  // bf16 q; the scale goes on the score
     c = a.cache_lens[cq.b];
     m = kNegInf;
     l = 0.f;
@@ -397,11 +420,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
     mbar_wait(&wbar[sk], (int)((hk / C::kSlots) & 1));
     mbar_wait(&wbar[sv], (int)(((hk + 1) / C::kSlots) & 1));
     const uint8_t *kst = ring + sk * C::kPageBytes, *vst = ring + sv * C::kPageBytes;
+#if DS_DEC_FAKE  // timing experiment only (wrong results): no compute on the pages
+    acc[0] += reinterpret_cast<const float *>(kst)[lane] + reinterpret_cast<const float *>(vst)[lane];
+    if (false)
+#else
     if (last)
-      consume_page<D, true>(kst, vst, q, acc, m, l, lane, cq.p * 16, c, a.k_new + row, a.v_new + row);
+#endif
+      consume_page<D, true>(kst, vst, qv, acc, m, l, lane, cq.p * 16, c, a.scale_log2, a.k_new + row,
+                            a.v_new + row);
     else
-      consume_page<D, false>(kst, vst, q, acc, m, l, lane, cq.p * 16, c, nullptr, nullptr);
-    // both half-stages consumed: refill them kSlots half-pages ahead
+      consume_page<D, false>(kst, vst, qv, acc, m, l, lane, cq.p * 16, c, a.scale_log2, nullptr, nullptr);
+    // both half-stages consumed: refill them kSlots half-pages ahead (refilling the
+    // K slot right after the score reads was measured slower)
     __syncwarp();
     if (lane == 0 && h_issued < h_end) {
       fence_proxy_async_smem();

@@ -43,7 +43,13 @@ constexpr uint32_t kChunkBytes128 = 128 * 128;  // Q: 128 rows x 128 B (64 bf16)
 constexpr uint32_t kChunkBytes64 = 64 * 128;    // K/V tile: 64 rows x 128 B per SW128 column block
 constexpr uint32_t kTmemCols = 256;             // S0 [0,64) S1 [64,128) O [128, 128+D)
 constexpr float kRescaleLog2 = 8.f;             // move the exponent base only past 2^8 growth
-constexpr int kPolyEvery = 8;                   // 1 in kPolyEvery exp2 on the FMA pipe (ex2_poly)
+#ifndef DS_PF_POLY_EVERY
+#define DS_PF_POLY_EVERY 8
+#endif
+#ifndef DS_PF_SLEEP_NS  // suspend hint of the producer / MMA waits (0: plain try_wait spin)
+#define DS_PF_SLEEP_NS 0
+#endif
+constexpr int kPolyEvery = DS_PF_POLY_EVERY;    // 1 in kPolyEvery exp2 on the FMA pipe (ex2_poly)
 
 template <int D>
 struct Smem {
@@ -87,6 +93,67 @@ enum {
 // -8 %, 16 x 2048 -3 %, 4 x 4096 -5 %, chunked prefill -5..7 %. (The MMA and
 // producer roles must stay under elect.sync: with a plain lane test the compiler
 // loses the uniform datapath for the UMMA operands and every length got slower.)
+#ifdef DS_TRACE
+// Timeline tracing (A/B builds only, tools/ab.sh trace "-DDS_TRACE"): clock64 stamps
+// of the role events of the CTAs that run on SM 0, read back with
+// ds_debug_prefill_trace (not part of the public ABI). Each recording thread owns a
+// region and a register counter, so a record is two plain stores (no atomics on
+// the timed path).
+constexpr int kTrSlots = 8, kTrRecorders = 8, kTrCap = 32768;
+__device__ unsigned long long g_pf_trace[kTrSlots * kTrRecorders * kTrCap * 2];
+__device__ unsigned int g_pf_slot;
+struct Tracer {
+  unsigned long long *base = nullptr;
+  uint32_t n = 0;
+  DS_DEVICE void rec(uint32_t ev, uint32_t cta, uint32_t g) {
+    if (base && n < kTrCap) {
+      base[2 * n] = clock64();
+      base[2 * n + 1] = ((uint64_t)ev << 56) | ((uint64_t)cta << 32) | g;
+      ++n;
+    }
+  }
+};
+#define TRACE(ev, g) tracer.rec((ev), cta_id, (g))
+#else
+#define TRACE(ev, g) ((void)0)
+#endif
+enum { T_SM_WAIT_S = 1, T_SM_GOT_S, T_SM_P_DONE, T_MMA_S, T_MMA_WAIT_P, T_MMA_PV, T_SM_EPI_DONE, T_LD_K, T_LD_V,
+       T_SM_WARP_P = 16 /* + warp */ };
+
+// Launch order of the work items (q tile i, head h, sequence r). The G = n_loc x
+// num_seqs (sequence, head) groups are cut into bands of a.band_groups groups whose
+// K/V fit comfortably in L2; inside a band the items go heaviest q tile first
+// ACROSS the band's groups (global longest-processing-time order, so the last
+// items of the launch are the cheapest and the persistent CTAs finish together),
+// while the K/V re-reads of a group stay within its band's time window (L2 hits).
+// band_groups = 1 is the plain group-major order.
+DS_DEVICE void item_coords(const PrefillArgs &a, int item, int &i, int &h, int &r) {
+  const int Q = a.num_q_tiles, G = a.n_loc * a.num_seqs, Gb = a.band_groups;
+  const int full = G / Gb, per_band = Gb * Q;
+  int band, k, gsz;
+  if (item < full * per_band) {
+    band = item / per_band;
+    k = item - band * per_band;
+    gsz = Gb;
+  } else {
+    band = full;
+    k = item - full * per_band;
+    gsz = G - full * Gb;
+  }
+  const int level = k / gsz, group = band * Gb + (k - level * gsz);
+  i = Q - 1 - level;
+  r = group / a.n_loc;
+  h = group - r * a.n_loc;
+}
+
+// waits of the producer and MMA threads
+DS_DEVICE void ctl_wait(uint64_t *bar, uint32_t parity) {
+  if (DS_PF_SLEEP_NS > 0)
+    mbar_wait_sleep(bar, parity, DS_PF_SLEEP_NS);
+  else
+    mbar_wait(bar, parity);
+}
+
 template <int D, bool kChunked>
 __global__ void __launch_bounds__(kThreads, 2)
     prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
@@ -126,7 +193,23 @@ __global__ void __launch_bounds__(kThreads, 2)
     tma_prefetch_desc(&tm_cache);
   }
 
-  int bx = blockIdx.x, by = blockIdx.y, bz = blockIdx.z;  // current item
+  int item = blockIdx.x;  // current item (linear launch index, see item_coords)
+#ifdef DS_TRACE
+  const uint32_t cta_id = blockIdx.x;
+  Tracer tracer;
+  {
+    __shared__ int tr_slot;
+    if (threadIdx.x == 0) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      tr_slot = smid == 0 ? (int)atomicAdd(&g_pf_slot, 1u) : -1;
+    }
+    __syncthreads();
+    const int rcd = warp < 4 ? warp : warp == 4 ? 4 : 5;  // softmax warps 0-3, producer, MMA
+    if (tr_slot >= 0 && tr_slot < kTrSlots && (lane == 0 || warp >= 4))
+      tracer.base = g_pf_trace + ((size_t)(tr_slot * kTrRecorders + rcd) * kTrCap) * 2;
+  }
+#endif
   uint32_t g0 = 0;  // kv tiles of earlier items (CTA-wide tile counter)
   uint32_t it = 0;  // non-empty items before the current one
   bool store_pending = false;  // producer: paged TMA stores may still read a stage
@@ -137,9 +220,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_arrive_expect_tx(&bars[B_CLC + (q & 1)], 16);
       clc_try_cancel(sbase + S::CLC + (q & 1) * 16, &bars[B_CLC + (q & 1)]);
     }
-    // item: q tiles of one (sequence, head) adjacent in launch order, heaviest first
-    const int h = by, r = bz;
-    const int i = a.num_q_tiles - 1 - bx;
+    int i, h, r;
+    item_coords(a, item, i, h, r);
     const int seq_start = a.cu_seqlens[r];
     const int len = a.cu_seqlens[r + 1] - seq_start;
     if (i * kBM < len) {
@@ -156,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ------------------------------------------------------------ producer
         __syncwarp();  // elect.sync needs the whole warp converged (lane 0 issued the CLC request)
         if (elect_one()) {
-          if (it > 0) mbar_wait(&bars[B_QE], (it - 1) & 1);  // the previous item's S MMAs are done with Q
+          if (it > 0) ctl_wait(&bars[B_QE], (it - 1) & 1);  // the previous item's S MMAs are done with Q
           mbar_arrive_expect_tx(&bars[B_Q], S::kQTile);
 #pragma unroll
           for (int c = 0; c < kChunks; ++c)
@@ -176,7 +258,7 @@ __global__ void __launch_bounds__(kThreads, 2)
               const uint32_t bytes = (uint32_t)np * 16 * D * 2;
 #pragma unroll
               for (int kv = 0; kv < 2; ++kv) {
-                if (g >= 2) mbar_wait(&bars[(kv ? B_VE : B_KE) + st], ph_free);
+                if (g >= 2) ctl_wait(&bars[(kv ? B_VE : B_KE) + st], ph_free);
                 uint64_t *full = &bars[(kv ? B_VF : B_KF) + st];
                 mbar_arrive_expect_tx(full, bytes);
                 for (int p = 0; p < np; ++p)
@@ -188,18 +270,20 @@ __global__ void __launch_bounds__(kThreads, 2)
               continue;
             }
             const int kv0 = seq_start + (j - npt) * kBN;
-            if (g >= 2) mbar_wait(&bars[B_KE + st], ph_free);  // S_{g-2} has consumed the K stage
+            if (g >= 2) ctl_wait(&bars[B_KE + st], ph_free);  // S_{g-2} has consumed the K stage
             mbar_arrive_expect_tx(&bars[B_KF + st], S::kKVTile);
 #pragma unroll
             for (int c = 0; c < kChunks; ++c)
               tma_load_3d(smem + S::K0 + st * S::kKVTile + c * kChunkBytes64, &tm_kv, &bars[B_KF + st], c * 64, h,
                           kv0);
-            if (g >= 2) mbar_wait(&bars[B_VE + st], ph_free);  // PV_{g-2} has consumed the V stage
+            TRACE(T_LD_K, g);
+            if (g >= 2) ctl_wait(&bars[B_VE + st], ph_free);  // PV_{g-2} has consumed the V stage
             mbar_arrive_expect_tx(&bars[B_VF + st], S::kKVTile);
 #pragma unroll
             for (int c = 0; c < kChunks; ++c)
               tma_load_3d(smem + S::V0 + st * S::kKVTile + c * kChunkBytes64, &tm_v, &bars[B_VF + st], c * 64, h,
                           kv0);
+            TRACE(T_LD_V, g);
           }
           // a3: the diagonal K/V tiles 2i (pages 8i..8i+3) and 2i+1 (8i+4..8i+7) -> paged
           // cache (chunked mode appends the chunk with ds' append kernel instead: the
@@ -209,8 +293,8 @@ __global__ void __launch_bounds__(kThreads, 2)
           for (int t = npt + 2 * i; npg > 0 && t < ntiles; ++t) {
             const uint32_t g = g0 + t;
             const int st = g & 1;
-            mbar_wait(&bars[B_KF + st], (g >> 1) & 1);
-            mbar_wait(&bars[B_VF + st], (g >> 1) & 1);
+            ctl_wait(&bars[B_KF + st], (g >> 1) & 1);
+            ctl_wait(&bars[B_VF + st], (g >> 1) & 1);
             for (int p = (t - npt - 2 * i) * 4; p < min(npg, (t - npt - 2 * i) * 4 + 4); ++p) {
               const int blk = bt[p];
 #pragma unroll
@@ -231,21 +315,20 @@ __global__ void __launch_bounds__(kThreads, 2)
       } else if (warp == 5) {
         // ------------------------------------------------------------ MMA issuer
         // Order per tile g: S_g = Q K_g^T, then O += P_{g-1} V_{g-1} (within an item).
-        // P.V completions are tracked per S buffer (B_O[g & 1]). mbarrier parity waits
-        // are exact only if the waiter has seen the previous phase of that barrier and
-        // the next one cannot have completed yet: this thread waits on P_k V_k for
-        // every k in order (k = g-2 before S_g, or at the end of the previous item)
-        // and always before issuing P_{k+2} V_{k+2}.
+        // P.V completions are tracked per S buffer (B_O[g & 1]) for the softmax warps;
+        // this thread never waits on them (in-order tcgen05.mma execution orders every
+        // S_g after the P_{g-2} V_{g-2} that reads its buffer).
         __syncwarp();
         if (elect_one()) {
           constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
           constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, D, 0, 1);
-          mbar_wait(&bars[B_Q], it & 1);
+          ctl_wait(&bars[B_Q], it & 1);
           auto issue_pv = [&](uint32_t g, bool first) {  // O (+)= P_g V_g
             const int st = g & 1;
-            mbar_wait(&bars[B_P + st], (g >> 1) & 1);
-            mbar_wait(&bars[B_VF + st], (g >> 1) & 1);
-            if (first && it > 0) mbar_wait(&bars[B_OE], (it - 1) & 1);  // previous item's O read out
+            TRACE(T_MMA_WAIT_P, g);
+            ctl_wait(&bars[B_P + st], (g >> 1) & 1);
+            ctl_wait(&bars[B_VF + st], (g >> 1) & 1);
+            if (first && it > 0) ctl_wait(&bars[B_OE], (it - 1) & 1);  // previous item's O read out
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < kBN / 16; ++kk)  // 16 keys = 8 packed P columns per step
@@ -254,14 +337,16 @@ __global__ void __launch_bounds__(kThreads, 2)
                       idesc_o, (!first || kk > 0));
             umma_commit(&bars[B_O + st]);
             umma_commit(&bars[B_VE + st]);
+            TRACE(T_MMA_PV, g);
           };
           for (int j = 0; j < ntiles; ++j) {
             const uint32_t g = g0 + j;
             const int st = g & 1;
-            mbar_wait(&bars[B_KF + st], (g >> 1) & 1);
-            // S buffer st still holds P_{g-2}: wait for P_{g-2} V_{g-2} (for j == 0 that
-            // wait already happened at the end of the previous item)
-            if (j >= 1 && g >= 2) mbar_wait(&bars[B_O + st], ((g >> 1) - 1) & 1);
+            ctl_wait(&bars[B_KF + st], (g >> 1) & 1);
+            // S buffer st still holds P_{g-2}, read by P_{g-2} V_{g-2}: that MMA was
+            // issued before this one by this thread, and tcgen05.mma ops of one thread
+            // execute in issue order, so S_g cannot overwrite P_{g-2} before it is read
+            // (no wait: the tensor pipe never drains between tiles)
             tc_fence_after();
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk)
@@ -272,10 +357,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                       idesc_s, kk > 0);
             umma_commit(&bars[B_SF + st]);
             umma_commit(&bars[B_KE + st]);
+            TRACE(T_MMA_S, g);
             if (j == ntiles - 1) umma_commit(&bars[B_QE]);
             if (j >= 1) issue_pv(g - 1, j == 1);
           }
-          if (gl >= 1) mbar_wait(&bars[B_O + ((gl - 1) & 1)], ((gl - 1) >> 1) & 1);  // frees S buffer gl+1
           issue_pv(gl, ntiles == 1);
         }
         __syncwarp();
@@ -295,7 +380,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int j = 0; j < ntiles; ++j) {
           const uint32_t g = g0 + j;
           const int st = g & 1;
+          if (threadIdx.x == 0) TRACE(T_SM_WAIT_S, g);
           mbar_wait(&bars[B_SF + st], (g >> 1) & 1);
+          if (threadIdx.x == 0) TRACE(T_SM_GOT_S, g);
           tc_fence_after();
           uint32_t sr[2][32];
           tmem_ld32(tmem + lane_off + st * kBN, sr[0]);
@@ -304,23 +391,27 @@ __global__ void __launch_bounds__(kThreads, 2)
           // row max on the raw scores (scale > 0 preserves order); prefix tiles: keys at
           // or beyond c0 are not cached yet (masked); chunk tiles: causal within the
           // chunk (key position > query position masked) — only the diagonal tiles
-          float mx = -__int_as_float(0x7f800000);
+          // row max on the raw scores; four independent 3-input max chains (the
+          // softmax is latency-bound with two softmax warps per SMSP, so ILP matters)
+          const float ninf = -__int_as_float(0x7f800000);
+          float mxv[4] = {ninf, ninf, ninf, ninf};
           const bool prefix_tail = kChunked && j == npt - 1 && (c0 % kBN) != 0;
           if (prefix_tail || j - npt >= 2 * i) {
             const int lim = prefix_tail ? c0 - 1 - j * kBN : q_pos - (j - npt) * kBN;  // last visible column
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
-              for (int e = 0; e < 32; ++e) {
+              for (int e = 0; e < 32; ++e)
                 if (cc * 32 + e > lim) sr[cc][e] = 0xff800000u;  // -inf
-                mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
-              }
-          } else {
-#pragma unroll
-            for (int cc = 0; cc < 2; ++cc)
-#pragma unroll
-              for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sr[cc][e]));
           }
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc)
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+              float &mk = mxv[(cc * 16 + e / 2) & 3];
+              mk = fmaxf(mk, fmaxf(__uint_as_float(sr[cc][e]), __uint_as_float(sr[cc][e + 1])));
+            }
+          const float mx = fmaxf(fmaxf(mxv[0], mxv[1]), fmaxf(mxv[2], mxv[3]));
           // Conditional rescaling: the exponent base m only moves when this tile's row
           // max exceeds it by more than kRescaleLog2 (p <= 2^8 in between, exact in
           // fp32/bf16 range); softmax is invariant to the base, so the result is the
@@ -334,23 +425,31 @@ __global__ void __launch_bounds__(kThreads, 2)
           // to bf16 (the P operand of the P.V MMA), the row sum stays fp32.
           uint32_t pk[32];
           const uint64_t sl2x2 = f2_pack(sl2, sl2), negm2 = f2_pack(-m_new, -m_new);
-          uint64_t rs2 = f2_pack(0.f, 0.f);
+          uint64_t rs2[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) rs2[u] = f2_pack(0.f, 0.f);
 #pragma unroll
           for (int cc = 0; cc < 2; ++cc)
 #pragma unroll
             for (int e = 0; e < 32; e += 2) {
               // exponent arguments two at a time (FFMA2); kPolyEvery-th exponentials on
               // the FMA pipe, the rest on MUFU; the fp32 row sum two at a time (FADD2)
+              // in four independent accumulators
               float x0, x1;
               f2_unpack(f2_fma(f2_pack(__uint_as_float(sr[cc][e]), __uint_as_float(sr[cc][e + 1])), sl2x2, negm2),
                         x0, x1);
+#if DS_PF_FAKE_EXP  // timing experiment only (wrong results): exp replaced by a clamp
+              const float p0 = fminf(x0, 1.f), p1 = fminf(x1, 1.f);
+#else
               const float p0 = (e % kPolyEvery) == 0 ? ex2_poly(x0) : ex2(x0);
               const float p1 = ((e + 1) % kPolyEvery) == 0 ? ex2_poly(x1) : ex2(x1);
-              rs2 = f2_add(rs2, f2_pack(p0, p1));
+#endif
+              uint64_t &rk = rs2[(cc * 16 + e / 2) & 3];
+              rk = f2_add(rk, f2_pack(p0, p1));
               pk[cc * 16 + e / 2] = pack_bf16(p0, p1);
             }
           float rs0, rs1;
-          f2_unpack(rs2, rs0, rs1);
+          f2_unpack(f2_add(f2_add(rs2[0], rs2[1]), f2_add(rs2[2], rs2[3])), rs0, rs1);
           l = l * alpha + (rs0 + rs1);
           m = m_new;
           if (j > 0 && __any_sync(0xffffffffu, grow)) {  // warp-uniform O rescale, only when a base moved
@@ -378,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive(&bars[B_P + st]);
+          if (lane == 0) TRACE(T_SM_WARP_P + warp, g);
         }
         // epilogue: O / l -> bf16 -> global (rows inside the sequence only)
         wait_pv(gl);
@@ -403,6 +503,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         tc_fence_before();
         mbar_arrive(&bars[B_OE]);  // the next item's first P.V may overwrite O
+        if (threadIdx.x == 0) TRACE(T_SM_EPI_DONE, gl);
       }
       g0 += ntiles;
       ++it;
@@ -415,9 +516,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(&bars[B_CLCE + (q & 1)]);
     if (!more) break;
-    bx = nx;
-    by = ny;
-    bz = nz;
+    item = nx;
   }
 
   if (warp == 4 && lane == 0 && g0 > 0) {
@@ -449,12 +548,45 @@ static cudaError_t launch_one(const PrefillArgs &a, const CUtensorMap &tq, const
                               const CUtensorMap &tv, const CUtensorMap &tc, cudaStream_t stream) {
   cudaError_t e = set_prefill_smem_once<D, C>();
   if (e != cudaSuccess) return e;
-  prefill_kernel<D, C><<<dim3(a.num_q_tiles, a.n_loc, a.num_seqs), kThreads, Smem<D>::ALLOC, stream>>>(tq, tk, tv,
-                                                                                                       tc, a);
+  prefill_kernel<D, C><<<a.num_q_tiles * a.n_loc * a.num_seqs, kThreads, Smem<D>::ALLOC, stream>>>(tq, tk, tv, tc, a);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+#ifdef DS_TRACE
+// copies the whole trace buffer (zero clock = empty record) and optionally clears it
+extern "C" __attribute__((visibility("default"))) int ds_debug_prefill_trace(unsigned long long *host, int cap_records,
+                                                                             int reset) {
+  const int total = kTrSlots * kTrRecorders * kTrCap;
+  cudaDeviceSynchronize();
+  if (host && cap_records >= total) cudaMemcpyFromSymbol(host, g_pf_trace, sizeof(g_pf_trace));
+  if (reset) {
+    void *p = nullptr;
+    cudaGetSymbolAddress(&p, g_pf_trace);
+    cudaMemset(p, 0, sizeof(g_pf_trace));
+    const unsigned int z = 0;
+    cudaMemcpyToSymbol(g_pf_slot, &z, sizeof(z));
+    cudaDeviceSynchronize();
+  }
+  return total;
+}
+#endif
+
+int prefill_band_groups(int max_kv_len, int head_dim) {
+  // bands of (sequence, head) groups whose K + V (max_kv_len x head_dim bf16 each)
+  // fit a DS_PREFILL_BAND_MB budget. Default 0 = one group per band, the plain
+  // group-major order: measured (tools/kernel_bench.py) as fast or faster than
+  // 8/32/64 MiB bands at every length (the tail of the launch is not where the
+  // time goes; the per-SM tensor/smem pipeline is).
+  static const long budget = [] {
+    const char *e = getenv("DS_PREFILL_BAND_MB");
+    return (e ? atol(e) : 0L) << 20;
+  }();
+  const long per_group = (long)max_kv_len * head_dim * 4;
+  const long g = budget / (per_group > 0 ? per_group : 1);
+  return g < 1 ? 1 : g > (1 << 20) ? (1 << 20) : (int)g;
+}
 
 bool prefill_persistent(int /*max_len*/) {
   // always (faster at every measured length); DS_PREFILL_PERSISTENT=0 runs one

@@ -45,6 +45,8 @@ struct Smem2 {
 
 enum { B_Q = 0, B_KF = 1, B_VF = 3, B_KE = 5, B_VE = 7, B_SF = 9, B_PF = 11, B_OD = 13 };  // [2]: stage / tile
 
+DS_DEVICE void ctl_wait2(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill2q_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -144,39 +146,46 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (elect_one()) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
       constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, D, 0, 1);
-      mbar_wait(&bars[B_Q], 0);
-      for (int j = 0; j < ntiles; ++j) {
+      // FA4-style order: S_A(0) S_B(0) | PV_A(j) S_A(j+1) PV_B(j) S_B(j+1) | ...
+      // so each tile's softmax overlaps the other tile's P.V and S MMAs (two MMA
+      // blocks). S_t(j+1) overwrites P_t(j) right after P_t(j) V_t(j) was issued:
+      // tcgen05.mma ops of one thread execute in issue order, so no wait is needed.
+      auto issue_s = [&](int t, int j) {
         const int st = j & 1;
-        mbar_wait(&bars[B_KF + st], (j >> 1) & 1);
+        if (t == 0 || j >= n_t(0)) ctl_wait2(&bars[B_KF + st], (j >> 1) & 1);  // first user of K_j waits
+        tc_fence_after();
+        const uint32_t qb = t ? S::QB : S::QA;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * kChunk + (kk & 3) * 32;
+          umma_ss(tS(t), smem_desc_sw128(sbase + qb + off, 16, 1024),
+                  smem_desc_sw128(sbase + S::K0 + st * S::kTile + off, 16, 1024), idesc_s, kk > 0);
+        }
+        umma_commit(&bars[B_SF + t]);
+        if (t == 1 || j >= n_t(1)) umma_commit(&bars[B_KE + st]);  // last user of K_j releases it
+      };
+      auto issue_pv = [&](int t, int j) {
+        const int st = j & 1;
+        ctl_wait2(&bars[B_PF + t], j & 1);
+        if (t == 0 || j >= n_t(0)) ctl_wait2(&bars[B_VF + st], (j >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          umma_ts(tO(t), tS(t) + kk * 8, smem_desc_sw128(sbase + S::V0 + st * S::kTile + kk * 16 * 128, kChunk, 1024),
+                  idesc_o, (j > 0 || kk > 0));
+        if (j == n_t(t) - 1) umma_commit(&bars[B_OD + t]);        // once per tile: O_t final
+        if (t == 1 || j >= n_t(1)) umma_commit(&bars[B_VE + st]);  // last user of V_j releases it
+      };
+      ctl_wait2(&bars[B_Q], 0);
+      issue_s(0, 0);
+      if (n_t(1) > 0) issue_s(1, 0);
+      for (int j = 0; j < ntiles; ++j) {
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           if (j >= n_t(t)) continue;
-          if (j >= 1) mbar_wait(&bars[B_OD + t], (j - 1) & 1);  // P_t(j-1), aliasing S_t, consumed
-          tc_fence_after();
-          const uint32_t qb = t ? S::QB : S::QA;
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            const uint32_t off = (kk >> 2) * kChunk + (kk & 3) * 32;
-            umma_ss(tS(t), smem_desc_sw128(sbase + qb + off, 16, 1024),
-                    smem_desc_sw128(sbase + S::K0 + st * S::kTile + off, 16, 1024), idesc_s, kk > 0);
-          }
-          umma_commit(&bars[B_SF + t]);
+          issue_pv(t, j);
+          if (j + 1 < n_t(t)) issue_s(t, j + 1);
         }
-        umma_commit(&bars[B_KE + st]);
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (j >= n_t(t)) continue;
-          mbar_wait(&bars[B_PF + t], j & 1);
-          mbar_wait(&bars[B_VF + st], (j >> 1) & 1);
-          tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk)
-            umma_ts(tO(t), tS(t) + kk * 8,
-                    smem_desc_sw128(sbase + S::V0 + st * S::kTile + kk * 16 * 128, kChunk, 1024), idesc_o,
-                    (j > 0 || kk > 0));
-          umma_commit(&bars[B_OD + t]);
-        }
-        umma_commit(&bars[B_VE + st]);
       }
     }
     __syncwarp();
@@ -189,7 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float sl2 = a.scale_log2;
     float m = -__int_as_float(0x7f800000), l = 0.f;
     for (int j = 0; j < n_t(t); ++j) {
-      // S_t(j) ready; it was issued after P_t(j-1) V_t(j-1) completed, so O_t is stable
+      // S_t(j) ready; it was issued after P_t(j-1) V_t(j-1), and in-order MMA
+      // execution means that P.V is complete too, so O_t is stable
       mbar_wait(&bars[B_SF + t], j & 1);
       tc_fence_after();
       uint32_t sr[4][32];
@@ -258,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&bars[B_PF + t]);
     }
     if (n_t(t) > 0) {
-      mbar_wait(&bars[B_OD + t], (n_t(t) - 1) & 1);
+      mbar_wait(&bars[B_OD + t], 0);  // committed once, after O_t's last P.V
       tc_fence_after();
       const float inv_l = 1.f / l;
       uint16_t *orow = reinterpret_cast<uint16_t *>(a.out) + ((size_t)(seq_start + q_pos) * a.n_loc + h) * D;

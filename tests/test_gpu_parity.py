@@ -604,3 +604,21 @@ def test_prefill_persistence_forced(force):
                         "(prefill or chunked or streamed or end_to_end) and not experimental and not forced"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("band_mb", ["0", "1"])
+def test_prefill_band_orders(band_mb):
+    """Launch-order bands (prefill_band_groups): DS_PREFILL_BAND_MB=0 is the plain
+    group-major order (one (sequence, head) group per band); 1 MiB gives bands of a
+    few groups and a partial last band at every parity shape. The item decode must
+    cover every (q tile, head, sequence) exactly once in either order."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, DS_PREFILL_BAND_MB=band_mb)
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_parity.py"), "-k",
+                        "(prefill or chunked) and not experimental and not forced and not band"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]

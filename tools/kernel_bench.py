@@ -9,17 +9,22 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("DS_PKG_ROOT"):  # an A/B variant build (tools/ab.sh)
+    sys.path.insert(0, os.path.abspath(os.environ["DS_PKG_ROOT"]))
 
 import numpy as np
 import torch
 
 import paper_2401_09670_b200 as ds
 
-PEAKS = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                    "MEASURED_PEAKS.json")))
+try:  # driver-measured on this pool; else the fallback B200_PROFILING.md states
+    PEAKS = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                        "MEASURED_PEAKS.json")))
+except OSError:
+    PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 
 
-def prefill_point(lens, n, d, reps=20, rot=4):
+def prefill_point(lens, n, d, reps=20, rot=4, warm=3, before_timed=None):
     T = sum(lens)
     bufs = [[torch.randn((T, n, d), device="cuda", dtype=torch.bfloat16) for _ in range(3)] for _ in range(rot)]
     out = torch.empty((T, n, d), device="cuda", dtype=torch.bfloat16)
@@ -32,10 +37,12 @@ def prefill_point(lens, n, d, reps=20, rot=4):
     tab_d = torch.from_numpy(tab).cuda()
     cu = torch.from_numpy(np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)).cuda()
     scale = 1 / math.sqrt(d)
-    for r in range(3):
+    for r in range(warm):
         q, k, v = bufs[r % rot]
         ds.ds_prefill_attn(q, k, v, out, cu, max(lens), cache, 0, tab_d, scale)
     torch.cuda.synchronize()
+    if before_timed:
+        before_timed()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for r in range(reps):
@@ -134,6 +141,10 @@ def main():
     if a.what in ("both", "prefill"):
         for lens in ([512] * 16, [512] * 64, [128] * 64, [1024] * 8, [2048] * 4, [2048] * 16, [4096] * 4):
             print(json.dumps(prefill_point(lens, a.n, a.d)), flush=True)
+        # config 5 (OPT-175B, TP4: 24 heads per GPU), LongBench-like prompts
+        rng = np.random.default_rng(0)
+        mix = [int(x) for x in rng.integers(1792, 1921, size=8)]
+        print(json.dumps(prefill_point(mix, 24, a.d)), flush=True)
     if a.what in ("both", "chunked"):
         for prefix in (0, 512, 1024, 1536):
             print(json.dumps(chunked_point(prefix, 512, 16, a.n, a.d)), flush=True)

@@ -1,5 +1,6 @@
 // Microbenchmark: MUFU ex2.approx.f32 vs FFMA throughput per SM on this GPU.
 #include <cstdio>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 __global__ void ex2_kernel(float *out, int iters, float seed) {
@@ -10,6 +11,21 @@ __global__ void ex2_kernel(float *out, int iters, float seed) {
     EX(a0) EX(a1) EX(a2) EX(a3) EX(a4) EX(a5) EX(a6) EX(a7)
   }
   out[blockIdx.x * blockDim.x + threadIdx.x] = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+}
+__global__ void ex2h2_kernel(float *out, int iters, float seed) {
+  // ex2.approx.f16x2: two exponentials per lane per instruction
+  unsigned a[8];
+  for (int j = 0; j < 8; ++j) {
+    __half2 h = __floats2half2_rn(-0.01f * (j + 1) + seed * 1e-3f, -0.02f * (j + 1));
+    a[j] = *reinterpret_cast<unsigned *>(&h);
+  }
+  for (int i = 0; i < iters; ++i) {
+#define EH(x) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(x));
+    EH(a[0]) EH(a[1]) EH(a[2]) EH(a[3]) EH(a[4]) EH(a[5]) EH(a[6]) EH(a[7])
+  }
+  unsigned s = 0;
+  for (int j = 0; j < 8; ++j) s ^= a[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __uint_as_float(s);
 }
 __global__ void ffma_kernel(float *out, int iters, float seed) {
   float a0 = seed + threadIdx.x * 1e-6f, a1 = a0 + 0.1f, a2 = a0 + 0.2f, a3 = a0 + 0.3f;
@@ -30,11 +46,12 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int iters = 20000, blocks = sms * 4, threads = 512;
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 3; ++k) {
     for (int w = 0; w < 2; ++w) {
       cudaEventRecord(e0);
       if (k == 0) ex2_kernel<<<blocks, threads>>>(out, iters, 0.5f);
-      else ffma_kernel<<<blocks, threads>>>(out, iters, 0.5f);
+      else if (k == 1) ffma_kernel<<<blocks, threads>>>(out, iters, 0.5f);
+      else ex2h2_kernel<<<blocks, threads>>>(out, iters, 0.5f);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
     }
@@ -43,7 +60,7 @@ int main() {
     double ops = double(blocks) * threads * iters * 8;
     double per_s = ops / (ms * 1e-3);
     // per SM per clock at the *current* clock is unknown; report per SM per ns and per clk at max clock
-    printf("%s: %.3f ms, %.1f Gop/s, %.2f op/clk/SM at max clock %d MHz\n", k == 0 ? "ex2.approx" : "ffma", ms,
+    printf("%s: %.3f ms, %.1f Gop/s, %.2f op/clk/SM at max clock %d MHz\n", k == 0 ? "ex2.approx.f32" : k == 1 ? "ffma" : "ex2.approx.f16x2 (instr; x2 values)", ms,
            per_s / 1e9, per_s / sms / (clk * 1e3), clk / 1000);
   }
   return 0;
