@@ -83,12 +83,13 @@ static PFN_encodeTiled get_encode() {
 }
 
 static ds_status encode(CUtensorMap *m, void *base, int rank, const cuuint64_t *dims,
-                        const cuuint64_t *strides_bytes, const cuuint32_t *box, const char *where) {
+                        const cuuint64_t *strides_bytes, const cuuint32_t *box, const char *where,
+                        CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_128B) {
   PFN_encodeTiled fn = get_encode();
   if (!fn) return fail(DS_ERR_CUDA, "%s: cuTensorMapEncodeTiled unavailable", where);
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, dims, strides_bytes, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DS_ERR_CUDA, "%s: cuTensorMapEncodeTiled failed (%d)", where, (int)r);
   return DS_OK;
@@ -100,6 +101,15 @@ static ds_status qkv_map(CUtensorMap *m, const void *p, int T, int n, int D, int
   const cuuint64_t str[2] = {(cuuint64_t)D * 2, (cuuint64_t)n * D * 2};
   const cuuint32_t box[3] = {64, 1, (cuuint32_t)rows};
   return encode(m, const_cast<void *>(p), 3, dims, str, box, where);
+}
+
+// prefill output [T][n][D]: box = 32 tokens x 32 dims of one head, unswizzled (the
+// epilogue of one softmax warp: its 32 q rows, one 32-column TMEM chunk at a time)
+static ds_status out_map(CUtensorMap *m, void *p, int T, int n, int D, const char *where) {
+  const cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)n, (cuuint64_t)T};
+  const cuuint64_t str[2] = {(cuuint64_t)D * 2, (cuuint64_t)n * D * 2};
+  const cuuint32_t box[3] = {32, 1, 32};
+  return encode(m, p, 3, dims, str, box, where, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
 // pool [L*2*NB][n][16][D]; box = one 16-token page x 64 dims
@@ -156,8 +166,9 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
   static const char *force = getenv("DS_PREFILL_KERNEL");
   const bool two_q = force && strcmp(force, "2q") == 0;
   const int kv_rows = two_q ? 128 : kPrefillKVRows;
-  CUtensorMap tq, tk, tv, tc;
+  CUtensorMap tq, tk, tv, tc, to;
   if (ds_status s = qkv_map(&tq, q, total_tokens, n, D, kPrefillQRows, W)) return s;
+  if (ds_status s = out_map(&to, out, total_tokens, n, D, W)) return s;
   if (ds_status s = qkv_map(&tk, k, total_tokens, n, D, kv_rows, W)) return s;
   if (ds_status s = qkv_map(&tv, v, total_tokens, n, D, kv_rows, W)) return s;
   if (ds_status s = cache_map(&tc, cache, W)) return s;
@@ -176,7 +187,7 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
   a.num_blocks = cache->num_blocks;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
   cudaError_t e = two_q ? launch_prefill2q(a, tq, tk, tv, tc, D, static_cast<cudaStream_t>(stream))
-                        : launch_prefill(a, tq, tk, tv, tc, D, static_cast<cudaStream_t>(stream));
+                        : launch_prefill(a, tq, tk, tv, tc, to, D, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, W);
   return DS_OK;
 }
@@ -204,8 +215,9 @@ extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const
     return fail(DS_ERR_INVALID_ARG, "%s: softmax_scale must be finite and > 0", W);
   if (ds_status s = require_sm100(W)) return s;
   const int D = cache->head_dim, n = cache->num_heads;
-  CUtensorMap tq, tk, tv, tc;
+  CUtensorMap tq, tk, tv, tc, to;
   if (ds_status s = qkv_map(&tq, q, total_tokens, n, D, kPrefillQRows, W)) return s;
+  if (ds_status s = out_map(&to, out, total_tokens, n, D, W)) return s;
   if (ds_status s = qkv_map(&tk, k, total_tokens, n, D, kPrefillKVRows, W)) return s;
   if (ds_status s = qkv_map(&tv, v, total_tokens, n, D, kPrefillKVRows, W)) return s;
   if (ds_status s = cache_map(&tc, cache, W)) return s;
@@ -224,7 +236,7 @@ extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const
   a.num_blocks = cache->num_blocks;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = launch_prefill(a, tq, tk, tv, tc, D, st);  // reads the prefix pages + the chunk
+  cudaError_t e = launch_prefill(a, tq, tk, tv, tc, to, D, st);  // reads the prefix pages + the chunk
   if (e != cudaSuccess) return cuda_fail(e, W);
   KvAppendArgs ap{};  // then the chunk's K/V join the pages (positions prefix + t)
   ap.k = static_cast<const uint16_t *>(k);

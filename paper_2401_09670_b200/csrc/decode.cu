@@ -314,6 +314,21 @@ DS_DEVICE void consume_page(const uint8_t *kst, const uint8_t *vst, const uint4 
   }
 }
 
+#ifdef DS_TRACE
+// per-warp globaltimer stamps (A/B trace builds only): entry, prefix built, first
+// page ready, loop done; read back with ds_debug_decode_trace
+__device__ unsigned long long g_dec_trace[kDecodeMaxSMs * kWarps][6];
+DS_DEVICE unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define DTRACE(k, v) \
+  if (lane == 0) g_dec_trace[blockIdx.x * kWarps + warp][k] = (v)
+#else
+#define DTRACE(k, v) ((void)0)
+#endif
+
 template <int D>
 __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs a) {
   using C = DecCfg<D>;
@@ -329,7 +344,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   // written by an earlier kernel (lengths, tables, pages, workspace) is read
   // before this wait.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  DTRACE(0, gtimer());
   build_prefix(a.cache_lens, B, prefix);
+  DTRACE(1, gtimer());
   const int64_t P = (int64_t)n * prefix[B];
   // at most one warp per page: every active warp range is non-empty, so a pair
   // never spans idle warps (tiny batches would otherwise merge across thousands)
@@ -419,6 +436,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
     }
     mbar_wait(&wbar[sk], (int)((hk / C::kSlots) & 1));
     mbar_wait(&wbar[sv], (int)(((hk + 1) / C::kSlots) & 1));
+#ifdef DS_TRACE
+    if (x == x0) DTRACE(2, gtimer());
+#endif
     const uint8_t *kst = ring + sk * C::kPageBytes, *vst = ring + sv * C::kPageBytes;
 #if DS_DEC_FAKE  // timing experiment only (wrong results): no compute on the pages
     acc[0] += reinterpret_cast<const float *>(kst)[lane] + reinterpret_cast<const float *>(vst)[lane];
@@ -476,9 +496,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
       advance(cq, prefix, n);
     }
   }
+  DTRACE(3, gtimer());
+  DTRACE(4, (unsigned long long)(x1 - x0));
 }
 
 }  // namespace
+
+#ifdef DS_TRACE
+extern "C" __attribute__((visibility("default"))) int ds_debug_decode_trace(unsigned long long *host, int reset) {
+  cudaDeviceSynchronize();
+  if (host) cudaMemcpyFromSymbol(host, g_dec_trace, sizeof(g_dec_trace));
+  if (reset) {
+    void *p = nullptr;
+    cudaGetSymbolAddress(&p, g_dec_trace);
+    cudaMemset(p, 0, sizeof(g_dec_trace));
+    cudaDeviceSynchronize();
+  }
+  return (int)(sizeof(g_dec_trace) / 8);
+}
+#endif
 
 size_t decode_partials_bytes(int head_dim, int num_sms) {
   return (size_t)num_sms * kWarps * 2 * (head_dim + 4) * sizeof(float);  // kPartialStride

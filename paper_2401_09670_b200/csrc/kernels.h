@@ -62,8 +62,8 @@ struct PrefillArgs {
   int32_t persistent;          // CTAs take over unlaunched CTAs' items (cluster launch control)
 };
 cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
-                           const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
-                           cudaStream_t stream);
+                           const CUtensorMap &tm_v, const CUtensorMap &tm_cache, const CUtensorMap &tm_o,
+                           int head_dim, cudaStream_t stream);
 size_t prefill_smem_bytes(int head_dim);
 int prefill_band_groups(int max_kv_len, int head_dim);  // L2-sized band of (sequence, head) groups
 bool prefill_persistent(int max_len);  // run the prefill CTAs persistently for this length?

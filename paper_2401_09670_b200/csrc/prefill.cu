@@ -58,7 +58,8 @@ struct Smem {
   static constexpr uint32_t Q = 0;
   static constexpr uint32_t K0 = Q + kQTile;           // 2 stages
   static constexpr uint32_t V0 = K0 + 2 * kKVTile;     // 2 stages
-  static constexpr uint32_t CLC = V0 + 2 * kKVTile;    // 2 x 16-B work-stealing responses
+  static constexpr uint32_t OST = V0 + 2 * kKVTile;    // epilogue staging: 4 warps x 32 rows x 32 dims bf16
+  static constexpr uint32_t CLC = OST + 4 * 2048;      // 2 x 16-B work-stealing responses
   static constexpr uint32_t BAR = CLC + 32;
   static constexpr uint32_t kBars = 21;
   static constexpr uint32_t TMEM_SLOT = BAR + kBars * 8;
@@ -158,7 +159,7 @@ template <int D, bool kChunked>
 __global__ void __launch_bounds__(kThreads, 2)
     prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_cache,
-                   const PrefillArgs a) {
+                   const __grid_constant__ CUtensorMap tm_o, const PrefillArgs a) {
   using S = Smem<D>;
   constexpr int kChunks = D / 64;
 
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     tma_prefetch_desc(&tm_kv);
     tma_prefetch_desc(&tm_v);
     tma_prefetch_desc(&tm_cache);
+    tma_prefetch_desc(&tm_o);
   }
 
   int item = blockIdx.x;  // current item (linear launch index, see item_coords)
@@ -479,26 +481,49 @@ __global__ void __launch_bounds__(kThreads, 2)
           mbar_arrive(&bars[B_P + st]);
           if (lane == 0) TRACE(T_SM_WARP_P + warp, g);
         }
-        // epilogue: O / l -> bf16 -> global (rows inside the sequence only)
+        // epilogue: O / l -> bf16 -> global. Each warp stages its 32 rows x 32 dims
+        // chunk in smem (2 KiB, 16-B pieces rotated by row pair: conflict-free
+        // STS) and one lane TMA-stores it: per-thread row stores (32 rows, 10 KB
+        // apart, per instruction) took ~5000 cycles per item on the LSU path. A
+        // warp whose rows run past the sequence end stores its valid rows directly
+        // (a TMA box would overwrite the next sequence's rows).
         wait_pv(gl);
         tc_fence_after();
         const float inv_l = 1.f / l;
+        const int row0 = i * kBM + warp * 32;
+        const bool boxed = row0 + 32 <= len;  // warp-uniform
+        uint8_t *stg = smem + S::OST + warp * 2048;
         uint16_t *orow = reinterpret_cast<uint16_t *>(a.out) + ((size_t)(seq_start + q_pos) * a.n_loc + h) * D;
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc) {
           uint32_t o[32];
           tmem_ld32(tO + lane_off + cc * 32, o);
           tmem_wait_ld();
-          if (q_pos < len) {
+          uint4 v[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              uint4 v;
-              v.x = pack_bf16(__uint_as_float(o[u * 8 + 0]) * inv_l, __uint_as_float(o[u * 8 + 1]) * inv_l);
-              v.y = pack_bf16(__uint_as_float(o[u * 8 + 2]) * inv_l, __uint_as_float(o[u * 8 + 3]) * inv_l);
-              v.z = pack_bf16(__uint_as_float(o[u * 8 + 4]) * inv_l, __uint_as_float(o[u * 8 + 5]) * inv_l);
-              v.w = pack_bf16(__uint_as_float(o[u * 8 + 6]) * inv_l, __uint_as_float(o[u * 8 + 7]) * inv_l);
-              *reinterpret_cast<uint4 *>(orow + cc * 32 + u * 8) = v;
+          for (int u = 0; u < 4; ++u) {
+            v[u].x = pack_bf16(__uint_as_float(o[u * 8 + 0]) * inv_l, __uint_as_float(o[u * 8 + 1]) * inv_l);
+            v[u].y = pack_bf16(__uint_as_float(o[u * 8 + 2]) * inv_l, __uint_as_float(o[u * 8 + 3]) * inv_l);
+            v[u].z = pack_bf16(__uint_as_float(o[u * 8 + 4]) * inv_l, __uint_as_float(o[u * 8 + 5]) * inv_l);
+            v[u].w = pack_bf16(__uint_as_float(o[u * 8 + 6]) * inv_l, __uint_as_float(o[u * 8 + 7]) * inv_l);
+          }
+          if (boxed) {
+            if (lane == 0) bulk_wait_group_read0();  // the previous chunk's store has read the buffer
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const int u = (k + (lane >> 1)) & 3;
+              *reinterpret_cast<uint4 *>(stg + lane * 64 + u * 16) = v[u];
             }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_3d(&tm_o, stg, cc * 32, h, seq_start + row0);
+              bulk_commit_group();
+            }
+          } else if (q_pos < len) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4 *>(orow + cc * 32 + u * 8) = v[u];
           }
         }
         tc_fence_before();
@@ -519,6 +544,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     item = nx;
   }
 
+  if (warp < 4 && lane == 0) bulk_wait_group0();  // the epilogue's O stores are complete
   if (warp == 4 && lane == 0 && g0 > 0) {
     // observe the last stage releases too (every mbarrier phase is waited on; also
     // guarantees the final MMAs have drained before the CTA retires)
@@ -545,10 +571,12 @@ static cudaError_t set_prefill_smem_once() {
 
 template <int D, bool C>
 static cudaError_t launch_one(const PrefillArgs &a, const CUtensorMap &tq, const CUtensorMap &tk,
-                              const CUtensorMap &tv, const CUtensorMap &tc, cudaStream_t stream) {
+                              const CUtensorMap &tv, const CUtensorMap &tc, const CUtensorMap &to,
+                              cudaStream_t stream) {
   cudaError_t e = set_prefill_smem_once<D, C>();
   if (e != cudaSuccess) return e;
-  prefill_kernel<D, C><<<a.num_q_tiles * a.n_loc * a.num_seqs, kThreads, Smem<D>::ALLOC, stream>>>(tq, tk, tv, tc, a);
+  prefill_kernel<D, C><<<a.num_q_tiles * a.n_loc * a.num_seqs, kThreads, Smem<D>::ALLOC, stream>>>(tq, tk, tv, tc, to,
+                                                                                                  a);
   return cudaGetLastError();
 }
 
@@ -603,14 +631,14 @@ size_t prefill_smem_bytes(int head_dim) {
 }
 
 cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
-                           const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
-                           cudaStream_t stream) {
+                           const CUtensorMap &tm_v, const CUtensorMap &tm_cache, const CUtensorMap &tm_o,
+                           int head_dim, cudaStream_t stream) {
   const bool chunked = a.prefix_lens != nullptr;
   if (head_dim == 128)
-    return chunked ? launch_one<128, true>(a, tm_q, tm_k, tm_v, tm_cache, stream)
-                   : launch_one<128, false>(a, tm_q, tm_k, tm_v, tm_cache, stream);
-  return chunked ? launch_one<64, true>(a, tm_q, tm_k, tm_v, tm_cache, stream)
-                 : launch_one<64, false>(a, tm_q, tm_k, tm_v, tm_cache, stream);
+    return chunked ? launch_one<128, true>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, stream)
+                   : launch_one<128, false>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, stream);
+  return chunked ? launch_one<64, true>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, stream)
+                 : launch_one<64, false>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, stream);
 }
 
 }  // namespace ds

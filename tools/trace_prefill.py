@@ -67,6 +67,14 @@ def main():
         v = np.array(v)
         print(f"{k:40s} n={len(v):6d} median={np.median(v):8.0f} p10={np.percentile(v, 10):8.0f} "
               f"p90={np.percentile(v, 90):8.0f}")
+    # epilogue: the item's last tile g (sm_epi_done recorded with g = last tile)
+    epi = []
+    for (c, gg), d in by.items():
+        if "sm_epi_done" in d and "P_last" in d:
+            epi.append(d["sm_epi_done"] - d["P_last"])
+    if epi:
+        print(f"{'epilogue (last P -> O stored)':40s} n={len(epi):6d} median={np.median(epi):8.0f} "
+              f"p90={np.percentile(epi, 90):8.0f}")
     # per-CTA tile rate
     per = collections.defaultdict(list)
     for (c, gg), d in by.items():
