@@ -103,13 +103,13 @@ static ds_status qkv_map(CUtensorMap *m, const void *p, int T, int n, int D, int
   return encode(m, const_cast<void *>(p), 3, dims, str, box, where);
 }
 
-// prefill output [T][n][D]: box = 32 tokens x 32 dims of one head, unswizzled (the
+// prefill output [T][n][D]: box = 32 tokens x 32 dims of one head, 64-B swizzle (the
 // epilogue of one softmax warp: its 32 q rows, one 32-column TMEM chunk at a time)
 static ds_status out_map(CUtensorMap *m, void *p, int T, int n, int D, const char *where) {
   const cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)n, (cuuint64_t)T};
   const cuuint64_t str[2] = {(cuuint64_t)D * 2, (cuuint64_t)n * D * 2};
   const cuuint32_t box[3] = {32, 1, 32};
-  return encode(m, p, 3, dims, str, box, where, CU_TENSOR_MAP_SWIZZLE_NONE);
+  return encode(m, p, 3, dims, str, box, where, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 // pool [L*2*NB][n][16][D]; box = one 16-token page x 64 dims

@@ -168,6 +168,9 @@ DS_DEVICE void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" 
 DS_DEVICE void bulk_wait_group_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+DS_DEVICE void bulk_wait_group_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 DS_DEVICE void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // 1-D bulk copy global -> shared completing on an mbarrier (size multiple of 16)

@@ -119,7 +119,8 @@ struct Tracer {
 #define TRACE(ev, g) ((void)0)
 #endif
 enum { T_SM_WAIT_S = 1, T_SM_GOT_S, T_SM_P_DONE, T_MMA_S, T_MMA_WAIT_P, T_MMA_PV, T_SM_EPI_DONE, T_LD_K, T_LD_V,
-       T_SM_WARP_P = 16 /* + warp */ };
+       T_SM_EPI_PV, T_EPI_LD = 32 /* 32 + 2*chunk: TMEM chunk loaded; +1: chunk stored */,
+       T_SM_WARP_P = 16 /* + warp (< 32) */ };
 
 // Launch order of the work items (q tile i, head h, sequence r). The G = n_loc x
 // num_seqs (sequence, head) groups are cut into bands of a.band_groups groups whose
@@ -482,39 +483,42 @@ __global__ void __launch_bounds__(kThreads, 2)
           if (lane == 0) TRACE(T_SM_WARP_P + warp, g);
         }
         // epilogue: O / l -> bf16 -> global. Each warp stages its 32 rows x 32 dims
-        // chunk in smem (2 KiB, 16-B pieces rotated by row pair: conflict-free
+        // chunk in smem (2 KiB in the 64-B swizzle of the TMA box: conflict-free
         // STS) and one lane TMA-stores it: per-thread row stores (32 rows, 10 KB
         // apart, per instruction) took ~5000 cycles per item on the LSU path. A
         // warp whose rows run past the sequence end stores its valid rows directly
         // (a TMA box would overwrite the next sequence's rows).
         wait_pv(gl);
+        if (threadIdx.x == 0) TRACE(T_SM_EPI_PV, gl);
         tc_fence_after();
         const float inv_l = 1.f / l;
         const int row0 = i * kBM + warp * 32;
         const bool boxed = row0 + 32 <= len;  // warp-uniform
         uint8_t *stg = smem + S::OST + warp * 2048;
         uint16_t *orow = reinterpret_cast<uint16_t *>(a.out) + ((size_t)(seq_start + q_pos) * a.n_loc + h) * D;
-#pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) {
-          uint32_t o[32];
-          tmem_ld32(tO + lane_off + cc * 32, o);
-          tmem_wait_ld();
+        const uint64_t inv2 = f2_pack(inv_l, inv_l), zero2 = f2_pack(0.f, 0.f);
+        auto store_chunk = [&](const uint32_t (&o)[32], int cc) {
           uint4 v[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            v[u].x = pack_bf16(__uint_as_float(o[u * 8 + 0]) * inv_l, __uint_as_float(o[u * 8 + 1]) * inv_l);
-            v[u].y = pack_bf16(__uint_as_float(o[u * 8 + 2]) * inv_l, __uint_as_float(o[u * 8 + 3]) * inv_l);
-            v[u].z = pack_bf16(__uint_as_float(o[u * 8 + 4]) * inv_l, __uint_as_float(o[u * 8 + 5]) * inv_l);
-            v[u].w = pack_bf16(__uint_as_float(o[u * 8 + 6]) * inv_l, __uint_as_float(o[u * 8 + 7]) * inv_l);
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float lo, hi;
+              f2_unpack(f2_fma(f2_pack(__uint_as_float(o[u * 8 + 2 * e]), __uint_as_float(o[u * 8 + 2 * e + 1])),
+                               inv2, zero2),
+                        lo, hi);
+              w[e] = pack_bf16(lo, hi);
+            }
+            v[u] = make_uint4(w[0], w[1], w[2], w[3]);
           }
           if (boxed) {
+            // (a second staging buffer per warp measured no faster)
             if (lane == 0) bulk_wait_group_read0();  // the previous chunk's store has read the buffer
             __syncwarp();
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int u = (k + (lane >> 1)) & 3;
-              *reinterpret_cast<uint4 *>(stg + lane * 64 + u * 16) = v[u];
-            }
+            for (int u = 0; u < 4; ++u)  // SWIZZLE_64B layout of the box: conflict-free STS
+              *reinterpret_cast<uint4 *>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = v[u];
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -525,6 +529,25 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
             for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4 *>(orow + cc * 32 + u * 8) = v[u];
           }
+          if (threadIdx.x == 0) TRACE(T_EPI_LD + 2 * cc + 1, gl);
+        };
+        // TMEM loads run one chunk ahead of the stores (two register buffers)
+        uint32_t oa[32], ob[32];
+        tmem_ld32(tO + lane_off, oa);
+        tmem_ld32(tO + lane_off + 32, ob);
+        tmem_wait_ld();
+        if (threadIdx.x == 0) TRACE(T_EPI_LD, gl);
+        store_chunk(oa, 0);
+        if constexpr (D == 128) {
+          tmem_ld32(tO + lane_off + 64, oa);
+          store_chunk(ob, 1);
+          tmem_wait_ld();
+          tmem_ld32(tO + lane_off + 96, ob);
+          store_chunk(oa, 2);
+          tmem_wait_ld();
+          store_chunk(ob, 3);
+        } else {
+          store_chunk(ob, 1);
         }
         tc_fence_before();
         mbar_arrive(&bars[B_OE]);  // the next item's first P.V may overwrite O

@@ -15,7 +15,7 @@ import kernel_bench as kb  # noqa: E402  (honours DS_PKG_ROOT)
 import paper_2401_09670_b200 as ds  # noqa: E402
 
 NAMES = {1: "sm_wait_S", 2: "sm_got_S", 3: "sm_P", 4: "mma_S", 5: "mma_wait_P", 6: "mma_PV", 7: "sm_epi_done",
-         8: "ld_K", 9: "ld_V"}
+         8: "ld_K", 9: "ld_V", 10: "sm_epi_pv"}
 
 
 def main():
@@ -42,6 +42,9 @@ def main():
     by = collections.defaultdict(dict)  # (cta, g) -> {event: clock}
     for c, e, gg, t in zip(cta, ev, g, clk):
         d = by[(c, gg)]
+        if 32 <= e < 48:
+            d[f"epi{e - 32}"] = t
+            continue
         if e >= 16:
             d["P_last"] = max(d.get("P_last", 0), t)
             d.setdefault("P_first", t)
@@ -72,6 +75,13 @@ def main():
     for (c, gg), d in by.items():
         if "sm_epi_done" in d and "P_last" in d:
             epi.append(d["sm_epi_done"] - d["P_last"])
+    epv = [d["sm_epi_pv"] - d["P_last"] for d in by.values() if "sm_epi_pv" in d and "P_last" in d]
+    if epv:
+        print(f"{'epilogue wait for last P.V':40s} n={len(epv):6d} median={np.median(epv):8.0f}")
+    for k in range(8):
+        a_ = [d[f"epi{k}"] - d["sm_epi_pv"] for d in by.values() if f"epi{k}" in d and "sm_epi_pv" in d]
+        if a_:
+            print(f"  epilogue chunk {k // 2} {'loaded' if k % 2 == 0 else 'stored'} at +{np.median(a_):.0f} after the P.V wait")
     if epi:
         print(f"{'epilogue (last P -> O stored)':40s} n={len(epi):6d} median={np.median(epi):8.0f} "
               f"p90={np.percentile(epi, 90):8.0f}")
