@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t cta_id = blockIdx.x;
   Tracer tracer;
   {
-    __shared__ int tr_slot;
+    int &tr_slot = *reinterpret_cast<int *>(smem + S::TMEM_SLOT + 8);  // spare bytes of the slot
     if (threadIdx.x == 0) {
       uint32_t smid;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
