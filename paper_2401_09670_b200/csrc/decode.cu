@@ -35,14 +35,20 @@ namespace ds {
 
 namespace {
 
-constexpr int kWarps = 16;
+#ifndef DS_DEC_WARPS
+#define DS_DEC_WARPS 16
+#endif
+#ifndef DS_DEC_SLOTS
+#define DS_DEC_SLOTS 3
+#endif
+constexpr int kWarps = DS_DEC_WARPS;  // consumer warps per CTA (one CTA per SM)
 constexpr int kMaxSeqs = kDecodeMaxSeqs;
 constexpr float kNegInf = -__builtin_huge_valf();
 
 template <int D>
 struct DecCfg {
   static constexpr int kPageBytes = 16 * D * 2;         // one K or V page of one head
-  static constexpr int kSlots = D == 128 ? 3 : 6;        // half-stages in flight per warp
+  static constexpr int kSlots = D == 128 ? DS_DEC_SLOTS : 2 * DS_DEC_SLOTS;  // half-stages per warp ring
   static constexpr int kRingBytes = kWarps * kSlots * kPageBytes;
   static constexpr int kPrefixOff = kRingBytes;          // int[kMaxSeqs + 1]
   static constexpr int kBarOff = (kPrefixOff + (kMaxSeqs + 1) * 4 + 7) & ~7;

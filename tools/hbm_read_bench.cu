@@ -3,6 +3,7 @@
 // vector loads and with 1-D TMA bulk copies into smem, and (b) device-to-device
 // copy (read + write, the MEASURED_PEAKS "copy" figure). 4 GiB buffers, > L2.
 #include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -116,10 +117,10 @@ __global__ void read_warps(const uint8_t *__restrict__ p, size_t bytes, int stri
   if (acc == 0x12345678u) *sink = acc;
 }
 
-int main() {
+int main(int argc, char **argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const size_t bytes = 4ull << 30;
+  const size_t bytes = argc > 1 ? (size_t)atoll(argv[1]) << 20 : 4ull << 30;  // MiB
   uint8_t *a, *b;
   unsigned long long *sink;
   cudaMalloc(&a, bytes);
