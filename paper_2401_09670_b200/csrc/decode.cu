@@ -316,6 +316,9 @@ DS_DEVICE void consume_page(const uint8_t *kst, const uint8_t *vst, const uint4 
     const float pw = __shfl_sync(0xffffffffu, p, g * TPG + it * 2);
     uint4 vv = *reinterpret_cast<const uint4 *>(vst + t * (D * 2) + dpart * 16);
     if (kLast && pos0 + t == c) vv = *reinterpret_cast<const uint4 *>(vnew);
+    // slots past position c hold whatever the pool held (never written for this
+    // sequence): their weight is 0, but 0 * NaN is NaN, so their V rows are zeroed
+    if (kLast && pos0 + t > c) vv = make_uint4(0u, 0u, 0u, 0u);
     axpy8(acc, pw, vv);
   }
 }

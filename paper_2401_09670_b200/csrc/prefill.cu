@@ -256,19 +256,24 @@ __global__ void __launch_bounds__(kThreads, 2)
             const int st = g & 1;
             const uint32_t ph_free = ((g >> 1) - 1) & 1;  // release of tile g-2 from this stage
             if (kChunked && j < npt) {
-              // prefix tile: up to 4 pages of 16 cached tokens straight from the pool
+              // prefix tile: 4 pages of 16 cached tokens straight from the pool. A tail
+              // tile with np < 4 prefix pages fills its remaining page slots with its
+              // last prefix page again: their keys are masked (p = 0 or ~2^-126), but
+              // the V rows still enter the P.V MMA, so they must be finite — stale smem
+              // (e.g. NaN patterns left by an earlier kernel) would poison the row.
               const int p0 = 4 * j, np = min(4, (c0 + 15) / 16 - p0);
-              const uint32_t bytes = (uint32_t)np * 16 * D * 2;
+              const uint32_t bytes = 4u * 16 * D * 2;
 #pragma unroll
               for (int kv = 0; kv < 2; ++kv) {
                 if (g >= 2) ctl_wait(&bars[(kv ? B_VE : B_KE) + st], ph_free);
                 uint64_t *full = &bars[(kv ? B_VF : B_KF) + st];
                 mbar_arrive_expect_tx(full, bytes);
-                for (int p = 0; p < np; ++p)
+                for (int p = 0; p < 4; ++p)
 #pragma unroll
                   for (int c = 0; c < kChunks; ++c)
                     tma_load_4d(smem + (kv ? S::V0 : S::K0) + st * S::kKVTile + c * kChunkBytes64 + p * 16 * 128,
-                                &tm_cache, full, c * 64, 0, h, (a.layer * 2 + kv) * a.num_blocks + btr[p0 + p]);
+                                &tm_cache, full, c * 64, 0, h,
+                                (a.layer * 2 + kv) * a.num_blocks + btr[p0 + min(p, np - 1)]);
               }
               continue;
             }

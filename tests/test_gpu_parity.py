@@ -32,9 +32,12 @@ def _ceil(a, b):
 class Side:
     """One pool (GPU + oracle mirror) with identical block tables."""
 
-    def __init__(self, oracle_mod, layers, num_blocks, heads, head_dim):
+    def __init__(self, oracle_mod, layers, num_blocks, heads, head_dim, poison=False):
         self.cache = ds.KVCache.empty(layers, num_blocks, heads, head_dim)
-        self.cache.tensor.zero_()
+        if poison:  # every never-written slot is a bf16 NaN (what reused pool memory may hold)
+            self.cache.tensor.view(torch.int16).fill_(0x7FC0)
+        else:
+            self.cache.tensor.zero_()
         self.pool = ds.Pool(num_blocks)
         self.opool = oracle_mod.Pool(layers, num_blocks, heads, head_dim)
 
@@ -146,7 +149,7 @@ def test_prefill_full_size_config2_sampled(oracle_mod):
 
 # ------------------------------------------------------------------ a7 + a8
 def run_decode(oracle_mod, ctx, n, d, seed=0, steps=1, fragment=0, q_sigma=1.0, max_cache_len=None,
-               table_cols=0):
+               table_cols=0, poison=False):
     """Prefill (GPU) the first ctx tokens of each sequence, then `steps` decode
     steps; compare each step with the oracle's decode."""
     B = len(ctx)
@@ -154,7 +157,7 @@ def run_decode(oracle_mod, ctx, n, d, seed=0, steps=1, fragment=0, q_sigma=1.0, 
     total = [c + steps for c in ctx]
     maxb = max(_ceil(max(total) + 1, BS), table_cols)
     nblocks = sum(_ceil(t + 1, BS) for t in total) + fragment + 4
-    side = Side(oracle_mod, 1, nblocks, n, d)
+    side = Side(oracle_mod, 1, nblocks, n, d, poison=poison)
     if fragment:
         side.fragment(seed + 7, fragment)
     t_ds = np.full((B, maxb), -1, np.int32)
@@ -210,6 +213,16 @@ def test_decode_parity(oracle_mod, ctx, n, d):
     side, table, cur, errs = run_decode(oracle_mod, ctx, n, d, seed=sum(ctx) % 97, steps=2, fragment=5)
     assert max(errs) <= TOL and max(errs) <= WARN, errs
     assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
+
+
+def test_decode_nan_poisoned_pool(oracle_mod):
+    """Slots past position c of a sequence's last page were never written for it
+    and may hold anything (here: bf16 NaN in every unwritten slot of the pool).
+    Their weight is 0, but 0 * NaN is NaN: the kernel must keep them out of P.V."""
+    for ctx, n in (([17, 5, 300], 2), ([543], 40), ([0, 1, 15], 1)):
+        side, table, cur, errs = run_decode(oracle_mod, ctx, n, 128, seed=5, steps=3, fragment=4, poison=True)
+        assert max(errs) <= WARN, (ctx, errs)
+        assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
 
 
 def test_decode_partition_invariance(oracle_mod):
@@ -531,13 +544,16 @@ def _chunked_round(oracle_mod, side, t_ds, t_or, prefix, chunk, n, d, seed):
     ([700, 5, 64], [130, 300, 1], 128),       # several prefix tiles, multi-tile chunks
     ([33, 250], [77, 129], 64),
 ])
-def test_chunked_prefill_parity(oracle_mod, prefix, chunk, d):
+@pytest.mark.parametrize("poison", [False, True])
+def test_chunked_prefill_parity(oracle_mod, prefix, chunk, d, poison):
     """NEXT-3: chunk attention over a paged prefix == the plain definition over
-    prefix + chunk (oracle), and the chunk's K/V are appended to the pages."""
+    prefix + chunk (oracle), and the chunk's K/V are appended to the pages. With
+    `poison` every never-written pool slot is a bf16 NaN: a prefix tail tile's
+    unused page slots must not reach the P.V MMA."""
     n = 4
     B = len(prefix)
     maxb = _ceil(max(p + c for p, c in zip(prefix, chunk)) + 1, BS)
-    side = Side(oracle_mod, 1, sum(_ceil(p + c, BS) for p, c in zip(prefix, chunk)) + 10, n, d)
+    side = Side(oracle_mod, 1, sum(_ceil(p + c, BS) for p, c in zip(prefix, chunk)) + 10, n, d, poison=poison)
     side.fragment(5, 6)
     t_ds = np.full((B, maxb), -1, np.int32)
     t_or = t_ds.copy()
