@@ -260,7 +260,7 @@ extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const
 extern "C" size_t ds_decode_workspace_bytes(int32_t num_seqs, int32_t n_loc, int32_t head_dim,
                                             int32_t max_cache_len) {
   if (num_seqs <= 0 || n_loc <= 0 || (head_dim != 64 && head_dim != 128) || max_cache_len < 0) return 0;
-  return decode_workspace_bytes(num_seqs, n_loc, head_dim, kDecodeMaxSMs);
+  return decode_layout(num_seqs, n_loc, head_dim, kDecodeMaxSMs, max_cache_len).total;
 }
 
 extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void *v_new, void *out,
@@ -297,8 +297,14 @@ extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void
   a.cache = static_cast<const uint16_t *>(cache->base);
   a.block_table = block_table;
   a.cache_lens = cache_lens;
-  a.workspace = static_cast<float *>(workspace);
-  a.tickets = reinterpret_cast<int32_t *>(static_cast<char *>(workspace) + decode_partials_bytes(D, kDecodeMaxSMs));
+  const DecodeLayout L = decode_layout(num_seqs, n, D, kDecodeMaxSMs, max_cache_len);
+  char *wsb = static_cast<char *>(workspace);
+  a.dyn = reinterpret_cast<int32_t *>(wsb + L.dyn_off);
+  a.workspace = reinterpret_cast<float *>(wsb + L.rows_off);
+  a.tickets = reinterpret_cast<int32_t *>(wsb + L.tickets_off);
+  a.chunk_rows = reinterpret_cast<float *>(wsb + L.chunk_off);
+  a.max_chunks = L.max_chunks;
+  a.max_cache_len = max_cache_len;
   a.layer = layer;
   a.num_blocks = cache->num_blocks;
   a.n_loc = n;

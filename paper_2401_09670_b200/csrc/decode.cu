@@ -42,6 +42,19 @@ namespace {
 #define DS_DEC_SLOTS 3
 #endif
 constexpr int kWarps = DS_DEC_WARPS;  // consumer warps per CTA (one CTA per SM)
+#ifndef DS_DEC_DYN_PCT
+#define DS_DEC_DYN_PCT 10
+#endif
+#ifndef DS_DEC_CHUNK
+#define DS_DEC_CHUNK 8
+#endif
+// Work split: each warp first streams a static contiguous page range; the last
+// kDynPct % of the pages are cut into chunks of kChunkPages that warps take
+// dynamically (one atomic counter) when their static range is done, so the warps
+// that stream slower (DRAM latency differs per SM) no longer set the launch's end.
+constexpr int kDynPct = DS_DEC_DYN_PCT;
+constexpr int kChunkPages = DS_DEC_CHUNK;
+constexpr int kRangeQ = 4;  // range queue entries per warp (the producer is < 2 pages ahead)
 constexpr int kMaxSeqs = kDecodeMaxSeqs;
 constexpr float kNegInf = -__builtin_huge_valf();
 
@@ -51,7 +64,9 @@ struct DecCfg {
   static constexpr int kSlots = D == 128 ? DS_DEC_SLOTS : 2 * DS_DEC_SLOTS;  // half-stages per warp ring
   static constexpr int kRingBytes = kWarps * kSlots * kPageBytes;
   static constexpr int kPrefixOff = kRingBytes;          // int[kMaxSeqs + 1]
-  static constexpr int kBarOff = (kPrefixOff + (kMaxSeqs + 1) * 4 + 7) & ~7;
+  static constexpr int kRangeOff = (kPrefixOff + (kMaxSeqs + 1) * 4 + 7) & ~7;  // int64[kWarps][kRangeQ][3]
+  static constexpr int kDoneOff = kRangeOff + kWarps * kRangeQ * 3 * 8;  // int: warps of this CTA done
+  static constexpr int kBarOff = kDoneOff + 8;
   static constexpr int kSmem = kBarOff + kWarps * kSlots * 8;
 };
 
@@ -94,7 +109,7 @@ DS_DEVICE void axpy8(float (&acc)[8], float p, const uint4 &v) {
 // weight of a partial with running max m against merged max mm (0 if empty)
 DS_DEVICE float rescale(float m, float mm) { return m == kNegInf ? 0.f : ex2(m - mm); }
 
-DS_DEVICE int npages_of(int c) { return (c + 1 + 15) >> 4; }
+__host__ __device__ inline int npages_of(int c) { return (c + 1 + 15) >> 4; }
 
 // page range [B_w, B_{w+1}) of warp w out of W over P pages
 __host__ __device__ inline int64_t range_begin(int64_t w, int64_t W, int64_t P) { return w * P / W; }
@@ -164,13 +179,42 @@ DS_DEVICE int64_t owner_of(int64_t x, int64_t W, int64_t P) {
   return w;
 }
 
+// The page space as "virtual workers": v < W are the static warp ranges over
+// [0, P1), v = W + c the dynamic chunk c over [P1 + c*kChunkPages, ...). Ranges are
+// contiguous, non-empty and in page order, so a (seq, head) pair's contributors
+// are the consecutive virtual workers owning its first .. last page.
+struct Part {
+  int64_t W, P1, P, NC;
+};
+__host__ __device__ inline Part make_part(int64_t P, int64_t Wmax, int64_t max_chunks) {
+  Part q;
+  q.W = P < Wmax ? P : Wmax;
+  int64_t dyn = 0;
+  // only with >= 64 pages per warp (measured: B = 128 and 256 x 544 tokens gain 5-7 %,
+  // B <= 64 loses up to 10 %: there the takes, the chunk partials and their merges
+  // cost more than the balance gains)
+  if (kDynPct > 0 && P >= 64 * q.W) dyn = (P * kDynPct / 100) / kChunkPages * kChunkPages;
+  if (dyn > max_chunks * kChunkPages) dyn = max_chunks * kChunkPages;  // workspace bound
+  q.P1 = P - dyn;
+  q.P = P;
+  q.NC = dyn / kChunkPages;
+  return q;
+}
+DS_DEVICE int64_t vbegin(const Part &q, int64_t v) {
+  return v <= q.W ? range_begin(v, q.W, q.P1) : q.P1 + (v - q.W) * kChunkPages;
+}
+DS_DEVICE int64_t vowner(const Part &q, int64_t x) {
+  return x < q.P1 ? owner_of(x, q.W, q.P1) : q.W + (x - q.P1) / kChunkPages;
+}
+
 // partial row of warp w, segment seg (0: its first pair, 1: its last pair):
 // o[D] then m, l; rows padded to 16 B so o loads/stores are vectors
 template <int D>
 constexpr int kPartialStride = D + 4;
 template <int D>
-DS_DEVICE float *partial_row(float *ws, int64_t w, int seg) {
-  return ws + ((size_t)w * 2 + seg) * kPartialStride<D>;
+DS_DEVICE float *partial_row(const DecodeArgs &a, const Part &q, int64_t v, int seg) {
+  return v < q.W ? a.workspace + ((size_t)v * 2 + seg) * kPartialStride<D>
+                 : a.chunk_rows + ((size_t)(v - q.W) * 2 + seg) * kPartialStride<D>;
 }
 
 // a8, fused: the warp that publishes the LAST partial of a straddling (seq, head)
@@ -180,12 +224,11 @@ DS_DEVICE float *partial_row(float *ws, int64_t w, int seg) {
 // them with an acquire fence through L2 (ld.cg). Every warp range is non-empty
 // (W <= P), so all k candidate contributors publish one partial each.
 template <int D>
-DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int h, int64_t W, int64_t P,
-                             int lane) {
+DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int h, const Part &part, int lane) {
   const int n = a.n_loc;
   const int npg = prefix[b + 1] - prefix[b];
   const int64_t start = (int64_t)n * prefix[b] + (int64_t)h * npg;
-  const int64_t w0 = owner_of(start, W, P), w1 = owner_of(start + npg - 1, W, P);
+  const int64_t w0 = vowner(part, start), w1 = vowner(part, start + npg - 1);
   const int k = (int)(w1 - w0 + 1);
   __syncwarp();  // the partial written by lanes < TPG is ordered before the release below
   int ticket = 0;
@@ -195,7 +238,7 @@ DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int 
   ticket = __shfl_sync(0xffffffffu, ticket, 0);
   if (ticket != k - 1) return;
   __syncwarp();
-  const int seg0 = range_begin(w0, W, P) < start ? 1 : 0;  // the pair is w0's last segment
+  const int seg0 = vbegin(part, w0) < start ? 1 : 0;  // the pair is w0's last segment
   constexpr int PER = D / 32;  // dims per lane: 4 (D = 128) or 2 (D = 64)
   constexpr int U = 8;         // contributors whose o slices are in flight at once
   float mm = kNegInf, lt = 0.f, ot[PER];
@@ -203,7 +246,7 @@ DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int 
   for (int e = 0; e < PER; ++e) ot[e] = 0.f;
   for (int j0 = 0; j0 < k; j0 += 32) {  // 32 contributors per round, (m, l) loads in parallel
     const int j = j0 + lane;
-    const float *ws = partial_row<D>(a.workspace, w0 + j, j == 0 ? seg0 : 0);
+    const float *ws = partial_row<D>(a, part, w0 + min(j, k - 1), j == 0 ? seg0 : 0);
     const float mj = j < k ? __ldcg(ws + D) : kNegInf;
     const float lj = j < k ? __ldcg(ws + D + 1) : 0.f;
     float mr = mj;
@@ -225,8 +268,8 @@ DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int 
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int jj = j0 + u0 + u;
-        const float *src = partial_row<D>(a.workspace, w0 + jj, jj == 0 ? seg0 : 0) + lane * PER;
         if (u0 + u < cnt) {
+          const float *src = partial_row<D>(a, part, w0 + jj, jj == 0 ? seg0 : 0) + lane * PER;
           if constexpr (PER == 4) {
             const float4 f = __ldcg(reinterpret_cast<const float4 *>(src));
             val[u][0] = f.x; val[u][1] = f.y; val[u][2] = f.z; val[u][3] = f.w;
@@ -338,7 +381,10 @@ DS_DEVICE unsigned long long gtimer() {
 #define DTRACE(k, v) ((void)0)
 #endif
 
-template <int D>
+// kDyn: the launch may take dynamic chunks (the host picks it when the batch can
+// reach >= 64 pages per warp); the static-only instance keeps the short path of
+// small batches free of the range queue (measured 1-3 us per launch at B <= 32).
+template <int D, bool kDyn>
 __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs a) {
   using C = DecCfg<D>;
   constexpr int TPG = D / 8;  // lanes per token row
@@ -353,26 +399,29 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   // written by an earlier kernel (lengths, tables, pages, workspace) is read
   // before this wait.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (threadIdx.x == 0) *reinterpret_cast<int *>(smem + C::kDoneOff) = 0;  // ordered by build_prefix's barriers
   DTRACE(0, gtimer());
   build_prefix(a.cache_lens, B, prefix);
   DTRACE(1, gtimer());
   const int64_t P = (int64_t)n * prefix[B];
   // at most one warp per page: every active warp range is non-empty, so a pair
   // never spans idle warps (tiny batches would otherwise merge across thousands)
-  const int64_t W = min((int64_t)gridDim.x * kWarps, P);
+  const Part part = make_part(P, (int64_t)gridDim.x * kWarps, kDyn ? a.max_chunks : 0);
+  const int64_t W = part.W;
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
   if (gw >= W) return;
-  const int64_t x0 = range_begin(gw, W, P), x1 = range_begin(gw + 1, W, P);
-  if (x0 >= x1) return;
 
   // per-warp ring of kSlots half-stages: slot 2k holds a K page, 2k+1 its V page
   uint8_t *ring = smem + warp * C::kSlots * C::kPageBytes;
   uint64_t *wbar = bars + warp * C::kSlots;
+  // per-warp queue of the page ranges this warp streams (its static range, then the
+  // dynamic chunks it took), written by the producer lane, read by the whole warp
+  int64_t *rq = reinterpret_cast<int64_t *>(smem + C::kRangeOff) + warp * 3 * kRangeQ;
   if (lane == 0) {
     for (int s = 0; s < C::kSlots; ++s) mbar_init(&wbar[s], 1);
     fence_barrier_init();
   }
-  __syncwarp();
+  __syncwarp();  // the barriers are initialised before any lane waits on them
 
   const size_t page_elems = 16 * D;
   const size_t kv_stride = (size_t)a.num_blocks * n * page_elems;  // K -> V
@@ -381,40 +430,85 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   // producer (lane 0): a page cursor that reads the block table one page ahead
   // (the load is consumed a step later, so lane 0 — and with it the consuming
   // warp — does not stall on it); the TMA bulk copies of K/V pages run kSlots
-  // half-pages ahead of the consumer. (An L2 prefetch of pages further ahead —
+  // half-pages ahead of the consumer. At the end of a range it continues with the
+  // chunk it took from the dynamic counter one range earlier (the atomic's result
+  // is not waited on until then). (An L2 prefetch of pages further ahead —
   // cp.async.bulk.prefetch or per-lane prefetch.global.L2 — was measured 10-40 %
   // SLOWER at every batch size and is not used.)
-  PagePos pf = locate(x0, prefix, B, n);
+  int nranges = 0;  // ranges written to the queue
+  int pend = (int)part.NC;
+  int64_t pr_x = 0, pr_x1 = 0;  // producer's next page / end of its current range
+  bool prod_done = false;
+  PagePos pf{};
   int blk_next = 0;
-  if (lane == 0) blk_next = a.block_table[(size_t)pf.b * a.max_blocks + pf.p];
-  int64_t x_pf = x0;
-  auto next_page = [&]() {  // pool offset (in pages) of page x_pf; advances the cursor
+  auto push_range = [&](int64_t v) {
+    const int64_t r0 = vbegin(part, v), r1 = vbegin(part, v + 1);
+    if (kDyn) {
+      int64_t *e = rq + 3 * (nranges % kRangeQ);
+      e[0] = r0;
+      e[1] = r1;
+      e[2] = v;
+      ++nranges;
+    }
+    pr_x = r0;
+    pr_x1 = r1;
+    pf = locate(r0, prefix, B, n);
+    blk_next = a.block_table[(size_t)pf.b * a.max_blocks + pf.p];
+  };
+  auto next_range = [&]() -> bool {
+    if (!kDyn) {
+      prod_done = true;
+      return false;
+    }
+    if (pend >= part.NC) {  // no chunk left: end-of-queue marker
+      rq[3 * (nranges % kRangeQ)] = -1;
+      ++nranges;
+      prod_done = true;
+      return false;
+    }
+    push_range(W + pend);
+    return true;
+  };
+  auto next_page = [&]() {  // pool offset (in pages) of page pr_x; advances the cursor
     const size_t off = (size_t)blk_next * n + pf.h;
-    if (++x_pf < x1) {
+    if (++pr_x < pr_x1) {
       advance(pf, prefix, n);
       blk_next = a.block_table[(size_t)pf.b * a.max_blocks + pf.p];
+    } else if (part.NC > 0) {
+      // the range's last page is being issued: take the next chunk now (its
+      // atomic completes while the ring still holds this range's last pages);
+      // once the counter is past the end nobody adds to it any more
+      pend = *reinterpret_cast<volatile int32_t *>(a.dyn) >= part.NC ? (int)part.NC : atomicAdd(a.dyn, 1);
     }
     return off;
   };
-  const int64_t h_end = 2 * (x1 - x0);  // half-pages of this warp
   int64_t h_issued = 0;
   const uint16_t *cur_page = nullptr;
-  auto issue = [&]() {
-    const int slot = (int)(h_issued % C::kSlots);
+  auto issue = [&]() -> bool {  // one half-page into the ring; false when nothing is left
     if ((h_issued & 1) == 0) {
+      if (pr_x == pr_x1 && !next_range()) return false;
       cur_page = layer_base + next_page() * page_elems;
     }
+    const int slot = (int)(h_issued % C::kSlots);
     mbar_arrive_expect_tx(&wbar[slot], C::kPageBytes);
     bulk_g2s(ring + slot * C::kPageBytes, cur_page + ((h_issued & 1) ? kv_stride : 0), C::kPageBytes,
              &wbar[slot]);
     ++h_issued;
+    return true;
   };
-  if (lane == 0)
-    while (h_issued < h_end && h_issued < C::kSlots) issue();
+  if (lane == 0) {
+    push_range(gw);
+    for (int i = 0; i < C::kSlots && issue(); ++i) {
+    }
+  }
 
-  // consumer
+  // consumer (its first range is the static one: computed here, not read from the
+  // queue, so its loads overlap the producer lane's)
+  int cr_i = 0;  // queue index of the range being consumed
+  const int64_t x0 = vbegin(part, gw);
+  int64_t cr_x1 = vbegin(part, gw + 1), cr_v = gw;
   PagePos cq = locate(x0, prefix, B, n);
-  int seg_begin = cq.p;  // the first segment may start mid-pair
+  int seg_begin = cq.p;  // the first segment of a range may start mid-pair
   bool first_seg = true;
   uint4 qv;
   float m = kNegInf, l = 0.f, acc[8];
@@ -431,8 +525,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   };
   load_pair();
 
-  for (int64_t x = x0; x < x1; ++x) {
-    const int64_t hk = 2 * (x - x0);
+  int64_t x = x0, xc = 0;  // page, and pages consumed by this warp so far
+  for (;; ++x, ++xc) {
+    const int64_t hk = 2 * xc;
     const int sk = (int)(hk % C::kSlots), sv = (int)((hk + 1) % C::kSlots);
     const bool last = cq.p == (c >> 4);
     if (last && lane < 2 * TPG) {  // (i) fused append of the new token at position c
@@ -446,7 +541,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
     mbar_wait(&wbar[sk], (int)((hk / C::kSlots) & 1));
     mbar_wait(&wbar[sv], (int)(((hk + 1) / C::kSlots) & 1));
 #ifdef DS_TRACE
-    if (x == x0) DTRACE(2, gtimer());
+    if (xc == 0) DTRACE(2, gtimer());
 #endif
     const uint8_t *kst = ring + sk * C::kPageBytes, *vst = ring + sv * C::kPageBytes;
 #if DS_DEC_FAKE  // timing experiment only (wrong results): no compute on the pages
@@ -462,13 +557,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
     // both half-stages consumed: refill them kSlots half-pages ahead (refilling the
     // K slot right after the score reads was measured slower)
     __syncwarp();
-    if (lane == 0 && h_issued < h_end) {
+    if (lane == 0 && !prod_done) {
       fence_proxy_async_smem();
-      issue();
-      if (h_issued < h_end) issue();
+      if (issue()) issue();
     }
     const bool pair_end = cq.p == cq.npg - 1;
-    if (pair_end || x == x1 - 1) {
+    const bool range_end = x == cr_x1 - 1;
+    if (pair_end || range_end) {
 #pragma unroll
       for (int off = TPG; off < 32; off <<= 1)  // sum the token-row groups (same m)
 #pragma unroll
@@ -484,7 +579,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
           *reinterpret_cast<uint4 *>(reinterpret_cast<uint16_t *>(a.out) + row) = o;
         }
       } else {  // a straddling pair: partial (o, m, l), merged by the last contributor (a8)
-        float *ws = partial_row<D>(a.workspace, gw, first_seg ? 0 : 1);
+        float *ws = partial_row<D>(a, part, cr_v, first_seg ? 0 : 1);
         if (lane < TPG) {
           reinterpret_cast<float4 *>(ws + dpart * 8)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
           reinterpret_cast<float4 *>(ws + dpart * 8)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
@@ -493,12 +588,25 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
             ws[D + 1] = l;
           }
         }
-        merge_if_last<D>(a, prefix, cq.b, cq.h, W, P, lane);
+        merge_if_last<D>(a, prefix, cq.b, cq.h, part, lane);
       }
       first_seg = false;
-      if (x + 1 < x1) {
+      if (!range_end) {
         advance(cq, prefix, n);
         seg_begin = 0;
+        load_pair();
+      } else {  // next range of this warp (its entry is written: the producer runs ahead)
+        if (!kDyn) break;
+        ++cr_i;
+        __syncwarp();
+        const int64_t *e = rq + 3 * (cr_i % kRangeQ);
+        if (e[0] < 0) break;
+        x = e[0] - 1;  // ++x at the loop head
+        cr_x1 = e[1];
+        cr_v = e[2];
+        cq = locate(e[0], prefix, B, n);
+        seg_begin = cq.p;
+        first_seg = true;
         load_pair();
       }
     } else {
@@ -506,7 +614,19 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
     }
   }
   DTRACE(3, gtimer());
-  DTRACE(4, (unsigned long long)(x1 - x0));
+  DTRACE(4, (unsigned long long)xc);
+  // the last warp out resets the dynamic counters for the next launch (every warp
+  // has made its final take by now); warps are counted per CTA in smem, and the
+  // last warp of each CTA counts the CTA globally (one global atomic per CTA)
+  if (part.NC > 0 && lane == 0) {
+    const int ctas = (int)((W + kWarps - 1) / kWarps);
+    const int in_cta = (int)min((int64_t)kWarps, W - (int64_t)blockIdx.x * kWarps);
+    int *cta_done = reinterpret_cast<int *>(smem + C::kDoneOff);
+    if (atomicAdd(cta_done, 1) == in_cta - 1 && atomicAdd(a.dyn + 1, 1) == ctas - 1) {
+      a.dyn[0] = 0;
+      a.dyn[1] = 0;
+    }
+  }
 }
 
 }  // namespace
@@ -525,20 +645,37 @@ extern "C" __attribute__((visibility("default"))) int ds_debug_decode_trace(unsi
 }
 #endif
 
-size_t decode_partials_bytes(int head_dim, int num_sms) {
-  return (size_t)num_sms * kWarps * 2 * (head_dim + 4) * sizeof(float);  // kPartialStride
-}
-size_t decode_workspace_bytes(int num_seqs, int n_loc, int head_dim, int num_sms) {
-  return decode_partials_bytes(head_dim, num_sms) + (size_t)num_seqs * n_loc * 4;  // + tickets
+// workspace: [dyn counters 16 B][static partial rows][tickets B x n][chunk partial rows]
+// (counters and tickets at offsets that do not depend on the lengths: they must
+// stay zero between calls; the chunk rows need no initialisation)
+DecodeLayout decode_layout(int num_seqs, int n_loc, int head_dim, int num_sms, int max_cache_len) {
+  DecodeLayout L;
+  const size_t row = (size_t)(head_dim + 4) * sizeof(float);
+  L.dyn_off = 0;
+  L.rows_off = 16;
+  L.tickets_off = L.rows_off + (size_t)num_sms * kWarps * 2 * row;
+  L.chunk_off = (L.tickets_off + (size_t)num_seqs * n_loc * 4 + 15) & ~(size_t)15;
+  const int64_t pmax = (int64_t)num_seqs * n_loc * npages_of(max_cache_len);
+  const Part q = make_part(pmax, (int64_t)num_sms * kWarps, INT64_MAX / kChunkPages);
+  L.max_chunks = q.NC;
+  L.total = L.chunk_off + (size_t)q.NC * 2 * row;
+  return L;
 }
 
 int decode_warps_per_cta() { return kWarps; }
 
-template <int D>
+template <int D, bool kDyn>
 static cudaError_t set_decode_smem_once() {
-  static cudaError_t st = cudaFuncSetAttribute(decode_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static cudaError_t st = cudaFuncSetAttribute(decode_kernel<D, kDyn>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                DecCfg<D>::kSmem);  // thread-safe static init, once
   return st;
+}
+template <int D, bool kDyn>
+static cudaError_t launch_d(cudaLaunchConfig_t &cfg, const DecodeArgs &a) {
+  cudaError_t e = set_decode_smem_once<D, kDyn>();
+  if (e != cudaSuccess) return e;
+  cfg.dynamicSmemBytes = DecCfg<D>::kSmem;
+  return cudaLaunchKernelEx(&cfg, decode_kernel<D, kDyn>, a);
 }
 
 cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaStream_t stream) {
@@ -551,16 +688,15 @@ cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaSt
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  // dynamic chunks only if the batch can reach the threshold (an upper bound of the
+  // page count from max_cache_len; the kernel decides exactly from the lengths)
+  const int64_t pmax = (int64_t)a.num_seqs * a.n_loc * npages_of(a.max_cache_len);
+  const bool dyn = a.max_chunks > 0 && make_part(pmax, (int64_t)num_sms * kWarps, a.max_chunks).NC > 0;
   cudaError_t e;
-  if (head_dim == 128) {
-    if ((e = set_decode_smem_once<128>()) != cudaSuccess) return e;
-    cfg.dynamicSmemBytes = DecCfg<128>::kSmem;
-    e = cudaLaunchKernelEx(&cfg, decode_kernel<128>, a);
-  } else {
-    if ((e = set_decode_smem_once<64>()) != cudaSuccess) return e;
-    cfg.dynamicSmemBytes = DecCfg<64>::kSmem;
-    e = cudaLaunchKernelEx(&cfg, decode_kernel<64>, a);
-  }
+  if (head_dim == 128)
+    e = dyn ? launch_d<128, true>(cfg, a) : launch_d<128, false>(cfg, a);
+  else
+    e = dyn ? launch_d<64, true>(cfg, a) : launch_d<64, false>(cfg, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

@@ -19,11 +19,18 @@ struct DecodeArgs {
   const int32_t *cache_lens;          // [B]
   float *workspace;                   // [warps][2][D+4] straddling-pair partials (o, m, l, pad)
   int32_t *tickets;                   // [B][n] merge tickets (zero between launches)
+  float *chunk_rows;                  // [chunks][2][D+4] partials of the dynamically taken chunks
+  int32_t *dyn;                       // [2]: chunk counter, finished warps (zero between launches)
+  int64_t max_chunks;                 // capacity of chunk_rows
+  int32_t max_cache_len;              // bound of cache_lens (host-side kernel choice)
   int32_t layer, num_blocks, n_loc, max_blocks, num_seqs;
   float scale_log2;  // softmax_scale * log2(e)
 };
-size_t decode_partials_bytes(int head_dim, int num_sms);
-size_t decode_workspace_bytes(int num_seqs, int n_loc, int head_dim, int num_sms);
+struct DecodeLayout {
+  size_t dyn_off, rows_off, tickets_off, chunk_off, total;
+  int64_t max_chunks;  // dynamic chunks the chunk rows hold
+};
+DecodeLayout decode_layout(int num_seqs, int n_loc, int head_dim, int num_sms, int max_cache_len);
 cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaStream_t stream);
 
 // a4 / a6: page rows <-> staging

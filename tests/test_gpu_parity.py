@@ -225,6 +225,18 @@ def test_decode_nan_poisoned_pool(oracle_mod):
         assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
 
 
+def test_decode_dynamic_chunks(oracle_mod):
+    """A batch big enough (>= 64 pages per warp) that the last 10 % of the pages
+    are taken dynamically in chunks by whichever warps finish their static range
+    first: results must not depend on who took what (two launches: oracle parity
+    and pages each time), and the self-resetting chunk counters must be ready for
+    the next launch (the second decode step reuses the workspace)."""
+    ctx = [int(x) for x in syn.rng(21).integers(300, 900, 512)]
+    side, table, cur, errs = run_decode(oracle_mod, ctx, 16, 128, seed=21, steps=2)
+    assert max(errs) <= WARN, errs
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
+
+
 def test_decode_partition_invariance(oracle_mod):
     """The page partition over warps depends on the whole batch: the same
     sequences decoded alone, inside a bigger batch, and with pages spread over
