@@ -54,6 +54,10 @@ constexpr int kWarps = DS_DEC_WARPS;  // consumer warps per CTA (one CTA per SM)
 // that stream slower (DRAM latency differs per SM) no longer set the launch's end.
 constexpr int kDynPct = DS_DEC_DYN_PCT;
 constexpr int kChunkPages = DS_DEC_CHUNK;
+#ifndef DS_DEC_DYN_MINPW
+#define DS_DEC_DYN_MINPW 64
+#endif
+constexpr int kDynMinPagesPerWarp = DS_DEC_DYN_MINPW;
 constexpr int kRangeQ = 4;  // range queue entries per warp (the producer is < 2 pages ahead)
 constexpr int kMaxSeqs = kDecodeMaxSeqs;
 constexpr float kNegInf = -__builtin_huge_valf();
@@ -193,7 +197,7 @@ __host__ __device__ inline Part make_part(int64_t P, int64_t Wmax, int64_t max_c
   // only with >= 64 pages per warp (measured: B = 128 and 256 x 544 tokens gain 5-7 %,
   // B <= 64 loses up to 10 %: there the takes, the chunk partials and their merges
   // cost more than the balance gains)
-  if (kDynPct > 0 && P >= 64 * q.W) dyn = (P * kDynPct / 100) / kChunkPages * kChunkPages;
+  if (kDynPct > 0 && P >= kDynMinPagesPerWarp * q.W) dyn = (P * kDynPct / 100) / kChunkPages * kChunkPages;
   if (dyn > max_chunks * kChunkPages) dyn = max_chunks * kChunkPages;  // workspace bound
   q.P1 = P - dyn;
   q.P = P;
