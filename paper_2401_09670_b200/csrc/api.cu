@@ -186,7 +186,7 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
   a.layer = layer;
   a.num_blocks = cache->num_blocks;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
-  cudaError_t e = two_q ? launch_prefill2q(a, tq, tk, tv, tc, D, static_cast<cudaStream_t>(stream))
+  cudaError_t e = two_q ? launch_prefill2q(a, tq, tk, tv, tc, to, D, static_cast<cudaStream_t>(stream))
                         : launch_prefill(a, tq, tk, tv, tc, to, D, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, W);
   return DS_OK;

@@ -76,7 +76,8 @@ int prefill_band_groups(int max_kv_len, int head_dim);  // L2-sized band of (seq
 bool prefill_persistent(int max_len);  // run the prefill CTAs persistently for this length?
 // experimental (DS_PREFILL_KERNEL=2q): two 128-row q tiles per CTA, 128-key tiles
 cudaError_t launch_prefill2q(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
-                             const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim, cudaStream_t stream);
+                             const CUtensorMap &tm_v, const CUtensorMap &tm_cache, const CUtensorMap &tm_o,
+                             int head_dim, cudaStream_t stream);
 
 // NEXT-3: append the chunk's K/V at positions prefix_lens[r] + t of each sequence
 struct KvAppendArgs {

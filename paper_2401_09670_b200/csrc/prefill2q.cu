@@ -1,8 +1,10 @@
 // prefill2q.cu — EXPERIMENTAL a2 + a3 variant (DS_PREFILL_KERNEL=2q): one CTA
 // per PAIR of 128-row q tiles (256 query rows) of one (sequence, head),
-// FA4-style ping-pong. Parity-tested; measured slower than prefill.cu's two
-// CTAs per SM (profiles/r01: 4x4096 821 us vs 683 us) because P aliases S in
-// TMEM, so S_t(j+1) must wait for P_t(j) V_t(j) and the per-tile chain grows.
+// FA4-style ping-pong with 128-key tiles. Parity-tested; still slower than
+// prefill.cu's two CTAs per SM (4 x 4096: 700 us vs 647-680 us, after the FA4
+// issue order and the TMA-store epilogue took it from 821 us): one CTA per SM
+// runs one item at a time (no persistence), so item start-up and the drain are
+// exposed, and each 128-column softmax tile is a long latency chain.
 //
 // Same computation as prefill.cu (§2.1, App. A;
 // readings R1, R2; a3 page write P:102):
@@ -37,7 +39,8 @@ struct Smem2 {
   static constexpr uint32_t QA = 0, QB = kTile;
   static constexpr uint32_t K0 = 2 * kTile;  // 2 stages
   static constexpr uint32_t V0 = K0 + 2 * kTile;
-  static constexpr uint32_t BAR = V0 + 2 * kTile;
+  static constexpr uint32_t OST = V0 + 2 * kTile;  // epilogue staging: 8 warps x 32 rows x 32 dims bf16
+  static constexpr uint32_t BAR = OST + 8 * 2048;
   static constexpr uint32_t kBars = 16;
   static constexpr uint32_t TMEM_SLOT = BAR + kBars * 8;
   static constexpr uint32_t ALLOC = TMEM_SLOT + 16 + 1024;
@@ -51,7 +54,7 @@ template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     prefill2q_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_cache,
-                     const PrefillArgs a) {
+                     const __grid_constant__ CUtensorMap tm_o, const PrefillArgs a) {
   using S = Smem2<D>;
   constexpr int kChunks = D / 64;
   const int h = blockIdx.y, r = blockIdx.z;
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t sbase = smem_u32(smem);
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + S::BAR);
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + S::TMEM_SLOT);
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int b = 0; b < (int)S::kBars; ++b) mbar_init(&bars[b], (b == B_PF || b == B_PF + 1) ? 128 : 1);
@@ -268,27 +271,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_arrive(&bars[B_PF + t]);
     }
     if (n_t(t) > 0) {
+      // epilogue as in prefill.cu: each warp stages its 32 rows x 32 dims chunks in
+      // smem (64-B swizzle of the TMA box) and one lane TMA-stores them; a warp whose
+      // rows run past the sequence end stores its valid rows directly
       mbar_wait(&bars[B_OD + t], 0);  // committed once, after O_t's last P.V
       tc_fence_after();
       const float inv_l = 1.f / l;
+      const int row0 = i * 2 * kBM + t * kBM + (warp & 3) * 32;
+      const bool boxed = row0 + 32 <= len;
+      uint8_t *stg = smem + S::OST + warp * 2048;
       uint16_t *orow = reinterpret_cast<uint16_t *>(a.out) + ((size_t)(seq_start + q_pos) * a.n_loc + h) * D;
 #pragma unroll
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t o[32];
         tmem_ld32(tO(t) + lane_off + cc * 32, o);
         tmem_wait_ld();
-        if (q_pos < len) {
+        uint4 v[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint4 v;
-            v.x = pack_bf16(__uint_as_float(o[u * 8 + 0]) * inv_l, __uint_as_float(o[u * 8 + 1]) * inv_l);
-            v.y = pack_bf16(__uint_as_float(o[u * 8 + 2]) * inv_l, __uint_as_float(o[u * 8 + 3]) * inv_l);
-            v.z = pack_bf16(__uint_as_float(o[u * 8 + 4]) * inv_l, __uint_as_float(o[u * 8 + 5]) * inv_l);
-            v.w = pack_bf16(__uint_as_float(o[u * 8 + 6]) * inv_l, __uint_as_float(o[u * 8 + 7]) * inv_l);
-            *reinterpret_cast<uint4 *>(orow + cc * 32 + u * 8) = v;
+        for (int u = 0; u < 4; ++u) {
+          v[u].x = pack_bf16(__uint_as_float(o[u * 8 + 0]) * inv_l, __uint_as_float(o[u * 8 + 1]) * inv_l);
+          v[u].y = pack_bf16(__uint_as_float(o[u * 8 + 2]) * inv_l, __uint_as_float(o[u * 8 + 3]) * inv_l);
+          v[u].z = pack_bf16(__uint_as_float(o[u * 8 + 4]) * inv_l, __uint_as_float(o[u * 8 + 5]) * inv_l);
+          v[u].w = pack_bf16(__uint_as_float(o[u * 8 + 6]) * inv_l, __uint_as_float(o[u * 8 + 7]) * inv_l);
+        }
+        if (boxed) {
+          if (lane == 0) bulk_wait_group_read0();
+          __syncwarp();
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<uint4 *>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = v[u];
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_3d(&tm_o, stg, cc * 32, h, seq_start + row0);
+            bulk_commit_group();
           }
+        } else if (q_pos < len) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4 *>(orow + cc * 32 + u * 8) = v[u];
         }
       }
+      if (lane == 0) bulk_wait_group0();
     }
   }
 
@@ -302,12 +325,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int D>
 static cudaError_t launch2(const PrefillArgs &a, const CUtensorMap &tq, const CUtensorMap &tk,
-                           const CUtensorMap &tv, const CUtensorMap &tc, cudaStream_t stream) {
+                           const CUtensorMap &tv, const CUtensorMap &tc, const CUtensorMap &to,
+                           cudaStream_t stream) {
   static cudaError_t attr = cudaFuncSetAttribute(prefill2q_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)Smem2<D>::ALLOC);
   if (attr != cudaSuccess) return attr;
   prefill2q_kernel<D><<<dim3(a.num_q_tiles, a.n_loc, a.num_seqs), kThreads, Smem2<D>::ALLOC, stream>>>(tq, tk, tv,
-                                                                                                       tc, a);
+                                                                                                       tc, to, a);
   return cudaGetLastError();
 }
 
@@ -315,10 +339,10 @@ static cudaError_t launch2(const PrefillArgs &a, const CUtensorMap &tq, const CU
 
 // a.num_q_tiles = number of q-tile PAIRS (256 rows); K/V maps with 128-row boxes
 cudaError_t launch_prefill2q(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
-                             const CUtensorMap &tm_v, const CUtensorMap &tm_cache, int head_dim,
-                             cudaStream_t stream) {
-  return head_dim == 128 ? launch2<128>(a, tm_q, tm_k, tm_v, tm_cache, stream)
-                         : launch2<64>(a, tm_q, tm_k, tm_v, tm_cache, stream);
+                             const CUtensorMap &tm_v, const CUtensorMap &tm_cache, const CUtensorMap &tm_o,
+                             int head_dim, cudaStream_t stream) {
+  return head_dim == 128 ? launch2<128>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, stream)
+                         : launch2<64>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, stream);
 }
 
 }  // namespace ds
