@@ -10,8 +10,10 @@ of B synthetic requests:
   a4-a6  ds_kv_migrate of all local layers' pages, prefill pool -> decode pool
   a7+a8  `output` decode steps x local layers of ds_decode_attn
 Default workload = BASELINE configs[1] (config 2): OPT-13B attention geometry
-(40 layers x 40 heads x 128), 64 requests x 512 prompt / 64 output (the decode
-batch a dedicated decode instance accumulates; SURVEY §8d sweeps B = 1..256).
+(40 layers x 40 heads x 128), 128 requests x 512 prompt / 64 output (the decode
+batch a dedicated decode instance accumulates — decoding is batched as far as
+memory allows, P:237; at N=1 both instances' pools, 2 x 56 GB, share the GPU;
+SURVEY §8d sweeps B = 1..256, profiles/r01/sweep_bench_c2_b*.json).
 At N=1 one GPU plays both instances (migration = LOCAL page copy); at N>1
 ranks [0, N/2) are prefill and [N/2, N) decode instances, paired by
 paper_2401_09670_b200.pairing (same layers/heads), migration = NCCL
@@ -51,7 +53,7 @@ NVLINK_GBS = 900.0  # nominal per direction per GPU (770 measured peer copy, B20
 CONFIGS = {
     "1": dict(geom=syn.TINY, mix="fixed", prompt=32, output=8, batch=1, tp=1, pp=1,
               desc="config 1: 1 layer x 4 heads x 64, prompt 32 + 8 decode steps"),
-    "2": dict(geom=syn.OPT_13B, mix="fixed", prompt=512, output=64, batch=64, tp=1, pp=1,
+    "2": dict(geom=syn.OPT_13B, mix="fixed", prompt=512, output=64, batch=128, tp=1, pp=1,
               desc="config 2: OPT-13B attention geometry, 512 in / 64 out"),
     "3": dict(geom=syn.OPT_13B, mix="chatbot", prompt=0, output=64, batch=64, tp=1, pp=1,
               desc="config 3: OPT-13B, ShareGPT-like chatbot length mix"),
