@@ -237,6 +237,18 @@ def test_decode_dynamic_chunks(oracle_mod):
     assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
 
 
+def test_decode_dynamic_chunks_ragged_d64(oracle_mod):
+    """The dynamic tail with head_dim 64 and a ragged batch: empty caches (c = 0),
+    one-page and many-page sequences, so chunks start and end inside pairs, cover
+    whole short pairs, and cross sequence boundaries."""
+    g = syn.rng(22)
+    ctx = [int(x) for x in g.integers(0, 1200, 700)]
+    ctx[:40] = [0] * 10 + [1] * 10 + [15] * 10 + [16] * 10
+    side, table, cur, errs = run_decode(oracle_mod, ctx, 24, 64, seed=22, steps=2, fragment=7)
+    assert max(errs) <= WARN, errs
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
+
+
 def test_decode_partition_invariance(oracle_mod):
     """The page partition over warps depends on the whole batch: the same
     sequences decoded alone, inside a bigger batch, and with pages spread over
