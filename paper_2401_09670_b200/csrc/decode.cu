@@ -215,8 +215,9 @@ DS_DEVICE int64_t vowner(const Part &q, int64_t x) {
 // o[D] then m, l; rows padded to 16 B so o loads/stores are vectors
 template <int D>
 constexpr int kPartialStride = D + 4;
-template <int D>
+template <int D, bool kDyn>
 DS_DEVICE float *partial_row(const DecodeArgs &a, const Part &q, int64_t v, int seg) {
+  if (!kDyn) return a.workspace + ((size_t)v * 2 + seg) * kPartialStride<D>;
   return v < q.W ? a.workspace + ((size_t)v * 2 + seg) * kPartialStride<D>
                  : a.chunk_rows + ((size_t)(v - q.W) * 2 + seg) * kPartialStride<D>;
 }
@@ -227,7 +228,7 @@ DS_DEVICE float *partial_row(const DecodeArgs &a, const Part &q, int64_t v, int 
 // Partials are published with a release fence + atomic ticket; the merger reads
 // them with an acquire fence through L2 (ld.cg). Every warp range is non-empty
 // (W <= P), so all k candidate contributors publish one partial each.
-template <int D>
+template <int D, bool kDyn>
 DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int h, const Part &part, int lane) {
   const int n = a.n_loc;
   const int npg = prefix[b + 1] - prefix[b];
@@ -250,7 +251,7 @@ DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int 
   for (int e = 0; e < PER; ++e) ot[e] = 0.f;
   for (int j0 = 0; j0 < k; j0 += 32) {  // 32 contributors per round, (m, l) loads in parallel
     const int j = j0 + lane;
-    const float *ws = partial_row<D>(a, part, w0 + min(j, k - 1), j == 0 ? seg0 : 0);
+    const float *ws = partial_row<D, kDyn>(a, part, w0 + min(j, k - 1), j == 0 ? seg0 : 0);
     const float mj = j < k ? __ldcg(ws + D) : kNegInf;
     const float lj = j < k ? __ldcg(ws + D + 1) : 0.f;
     float mr = mj;
@@ -272,8 +273,8 @@ DS_DEVICE void merge_if_last(const DecodeArgs &a, const int *prefix, int b, int 
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int jj = j0 + u0 + u;
+        const float *src = partial_row<D, kDyn>(a, part, w0 + min(jj, k - 1), jj == 0 ? seg0 : 0) + lane * PER;
         if (u0 + u < cnt) {
-          const float *src = partial_row<D>(a, part, w0 + jj, jj == 0 ? seg0 : 0) + lane * PER;
           if constexpr (PER == 4) {
             const float4 f = __ldcg(reinterpret_cast<const float4 *>(src));
             val[u][0] = f.x; val[u][1] = f.y; val[u][2] = f.z; val[u][3] = f.w;
@@ -583,7 +584,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
           *reinterpret_cast<uint4 *>(reinterpret_cast<uint16_t *>(a.out) + row) = o;
         }
       } else {  // a straddling pair: partial (o, m, l), merged by the last contributor (a8)
-        float *ws = partial_row<D>(a, part, cr_v, first_seg ? 0 : 1);
+        float *ws = partial_row<D, kDyn>(a, part, cr_v, first_seg ? 0 : 1);
         if (lane < TPG) {
           reinterpret_cast<float4 *>(ws + dpart * 8)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
           reinterpret_cast<float4 *>(ws + dpart * 8)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
             ws[D + 1] = l;
           }
         }
-        merge_if_last<D>(a, prefix, cq.b, cq.h, part, lane);
+        merge_if_last<D, kDyn>(a, prefix, cq.b, cq.h, part, lane);
       }
       first_seg = false;
       if (!range_end) {
