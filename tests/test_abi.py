@@ -160,6 +160,22 @@ def test_decode_validation_and_workspace():
     assert call(543, FAKE, ws) == ds.DS_ERR_CUDA
 
 
+def test_decode_workspace_holds_the_dynamic_chunks():
+    """The workspace grows with the batch's page count once the dynamic tail is on
+    (>= 64 pages per warp of the largest grid: 160 SMs x 16 warps): 10 % of the
+    pages in 8-page chunks, two (D + 4)-float partial rows per chunk."""
+    f = ds.ds_decode_workspace_bytes
+    # 64 x 40 x 35 pages stay static: the size does not depend on the lengths
+    assert f(64, 40, 128, 1000) == f(64, 40, 128, 543)
+    big_b = 1024
+    pages = big_b * 40 * ((543 + 1 + 15) // 16)
+    assert pages >= 64 * 160 * 16
+    chunks = (pages * 10 // 100) // 8
+    base = f(big_b, 40, 128, 0)  # one page per sequence: static
+    assert f(big_b, 40, 128, 543) == base + chunks * 2 * (128 + 4) * 4
+    assert f(big_b, 40, 128, 1000) > f(big_b, 40, 128, 543)  # more pages -> more chunk rows
+
+
 def test_staging_sizes():
     c = _cache(L=40, NB=1000, n=40, D=128)
     assert ds.lib().ds_kv_staging_bytes(ctypes.byref(c), 40, 32, 40) == 40 * 2 * 32 * 40 * 4096
