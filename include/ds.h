@@ -13,6 +13,8 @@
  * This header is the whole boundary of the hot path:
  *   a1  ds_block_table      page allocation / block tables (host)
  *   a2+a3 ds_prefill_attn   causal prefill attention + paged K/V write
+ *   a2-a6 ds_prefill_attn_push  the same with the migration fused in (pages
+ *                           stored straight into the decoding instance's pool)
  *   a4  ds_kv_pack          gather pages of a head slice into a staging buffer
  *   a5  ds_kv_migrate       pack -> NCCL send/recv over NVLink -> unpack
  *   a6  ds_kv_unpack        scatter a staging buffer into pages
@@ -136,6 +138,35 @@ ds_status ds_prefill_attn(const void *q, const void *k, const void *v, void *out
                           const ds_kv_cache *cache, int32_t layer,
                           const int32_t *block_table, int32_t max_blocks_per_seq,
                           float softmax_scale, void *stream);
+
+/* ======================================================================
+ * a2 + a3 + a4-a6 fused — prefill with the page migration inside the kernel
+ * ("push"): as ds_prefill_attn, and every K/V page the kernel writes is also
+ * stored, from the same shared-memory tile, into a DESTINATION pool — the
+ * decoding instance's ("the decode instance receives the KV caches"),
+ * either a peer GPU's pool mapped with ds_ipc_open_mem (the stores cross NVLink
+ * while the attention of later tiles runs) or another pool of this GPU:
+ *   dst[dst_layer][K|V][dst_block_table[r][t/16]][dst_head0 + h][t%16] = k|v[t][h]
+ * The decoding side must have admitted the batch (allocated its pages) before
+ * the call — the paper's pull lets the prefill GPU buffer the pages
+ * until the decoder has memory; this push is the variant for a decoder that
+ * already has it, and costs no separate migration pass.
+ * dst_cache      : host descriptor of the destination pool (base may be a
+ *                  peer-mapped pointer); same head_dim and block size;
+ *                  dst_head0 + n_loc <= dst_cache->num_heads.
+ * dst_block_table: device int32 [num_seqs][dst_max_blocks_per_seq] (this
+ *                  GPU's memory), ceil(l_r/16) valid destination page ids per row.
+ * write_local    : 1 also writes the source pool as ds_prefill_attn does;
+ *                  0 writes the pages only to the destination.
+ * Errors as ds_prefill_attn, plus DS_ERR_INVALID_ARG for a bad destination.
+ * ==================================================================== */
+ds_status ds_prefill_attn_push(const void *q, const void *k, const void *v, void *out,
+                               const int32_t *cu_seqlens, int32_t num_seqs, int32_t total_tokens,
+                               int32_t max_seqlen, const ds_kv_cache *cache, int32_t layer,
+                               const int32_t *block_table, int32_t max_blocks_per_seq,
+                               const ds_kv_cache *dst_cache, int32_t dst_layer,
+                               const int32_t *dst_block_table, int32_t dst_max_blocks_per_seq,
+                               int32_t dst_head0, int32_t write_local, float softmax_scale, void *stream);
 
 /* ======================================================================
  * NEXT-3 — chunked prefill over a paged prefix, the technique the

@@ -31,7 +31,7 @@ EXPORTED = (
     "ds_kv_staging_bytes", "ds_kv_pack", "ds_kv_unpack", "ds_comm_get_unique_id", "ds_comm_init",
     "ds_comm_destroy", "ds_kv_migrate_staging_bytes", "ds_kv_migrate", "ds_ipc_export_mem", "ds_ipc_open_mem",
     "ds_ipc_close_mem", "ds_event_create_ipc", "ds_event_open_ipc", "ds_event_record", "ds_event_wait",
-    "ds_event_destroy", "ds_prefill_attn_chunked",
+    "ds_event_destroy", "ds_prefill_attn_chunked", "ds_prefill_attn_push",
 )
 
 
@@ -62,6 +62,8 @@ def _load():
         "ds_pool_num_free": ([P, ctypes.POINTER(i32)], ctypes.c_int),
         "ds_block_table": ([P, i32, i32, P, P, P, i32, i32, ctypes.POINTER(i32)], ctypes.c_int),
         "ds_prefill_attn": ([P, P, P, P, P, i32, i32, i32, cache_p, i32, P, i32, f32, P], ctypes.c_int),
+        "ds_prefill_attn_push": ([P, P, P, P, P, i32, i32, i32, cache_p, i32, P, i32, cache_p, i32, P, i32, i32, i32,
+                                  f32, P], ctypes.c_int),
         "ds_prefill_attn_chunked": ([P, P, P, P, P, P, i32, i32, i32, i32, cache_p, i32, P, i32, f32, P],
                                     ctypes.c_int),
         "ds_decode_workspace_bytes": ([i32, i32, i32, i32], sz),
@@ -236,6 +238,31 @@ def ds_prefill_attn(q, k, v, out, cu_seqlens, max_seqlen: int, cache: KVCache, l
                                 cu_seqlens.data_ptr(), cu_seqlens.numel() - 1, T, max_seqlen,
                                 cache.ref(), layer, block_table.data_ptr(), block_table.shape[1],
                                 softmax_scale, _stream(stream)))
+
+
+def ds_prefill_attn_push(q, k, v, out, cu_seqlens, max_seqlen: int, cache: KVCache, layer: int, block_table,
+                         dst_cache: KVCache, dst_layer: int, dst_block_table, softmax_scale: float,
+                         dst_head0: int = 0, write_local: bool = True, stream=None, total_tokens: int | None = None):
+    """a2-a6 fused: prefill whose page stores also land in `dst_cache` (the
+    decoding instance's pool; a peer GPU's pool mapped through IPC or a pool of
+    this GPU) at `dst_layer` / `dst_block_table` / `dst_head0`."""
+    torch = _torch()
+    for t, nm in ((q, "q"), (k, "k"), (v, "v"), (out, "out")):
+        _dev(t, torch.bfloat16, nm)
+    _dev(cu_seqlens, torch.int32, "cu_seqlens")
+    _dev(block_table, torch.int32, "block_table")
+    _dev(dst_block_table, torch.int32, "dst_block_table")
+    T = q.shape[0] if total_tokens is None else total_tokens
+    if q.dim() != 3 or q.shape[1] != cache.heads or q.shape[2] != cache.head_dim:
+        raise ValueError("q must be [T][n_loc][head_dim] matching the cache")
+    for t in (k, v, out):
+        if t.shape != q.shape:
+            raise ValueError("q, k, v, out must have the same shape")
+    _check(_lib.ds_prefill_attn_push(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+                                     cu_seqlens.data_ptr(), cu_seqlens.numel() - 1, T, max_seqlen, cache.ref(), layer,
+                                     block_table.data_ptr(), block_table.shape[1], dst_cache.ref(), dst_layer,
+                                     dst_block_table.data_ptr(), dst_block_table.shape[1], dst_head0,
+                                     1 if write_local else 0, softmax_scale, _stream(stream)))
 
 
 def ds_prefill_attn_chunked(q, k, v, out, cu_seqlens, prefix_lens, max_chunk_len: int, max_context_len: int,

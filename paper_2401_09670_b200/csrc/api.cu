@@ -137,24 +137,41 @@ using namespace ds;
 
 extern "C" const char *ds_last_error(void) { return g_last_error.c_str(); }
 
-extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v, void *out,
-                                     const int32_t *cu_seqlens, int32_t num_seqs,
-                                     int32_t total_tokens, int32_t max_seqlen,
-                                     const ds_kv_cache *cache, int32_t layer,
-                                     const int32_t *block_table, int32_t max_blocks_per_seq,
-                                     float softmax_scale, void *stream) {
-  const char *W = "ds_prefill_attn";
+// Push target of the fused prefill + migration (nullptr: plain prefill).
+struct PushTarget {
+  const ds_kv_cache *cache;
+  int32_t layer;
+  const int32_t *block_table;
+  int32_t max_blocks, head0, write_local;
+};
+
+static ds_status prefill_impl(const char *W, const void *q, const void *k, const void *v, void *out,
+                              const int32_t *cu_seqlens, int32_t num_seqs, int32_t total_tokens,
+                              int32_t max_seqlen, const ds_kv_cache *cache, int32_t layer,
+                              const int32_t *block_table, int32_t max_blocks_per_seq, float softmax_scale,
+                              const PushTarget *push, void *stream) {
   if (num_seqs < 0) return fail(DS_ERR_INVALID_ARG, "%s: num_seqs < 0", W);
   if (ds_status s = check_cache(cache, W)) return s;
+  if (push) {
+    if (ds_status s = check_cache(push->cache, W)) return s;
+    if (push->cache->head_dim != cache->head_dim)
+      return fail(DS_ERR_INVALID_ARG, "%s: destination pool head_dim differs", W);
+    if (push->layer < 0 || push->layer >= push->cache->num_layers)
+      return fail(DS_ERR_INVALID_ARG, "%s: dst_layer out of range", W);
+    if (push->head0 < 0 || push->head0 + cache->num_heads > push->cache->num_heads)
+      return fail(DS_ERR_INVALID_ARG, "%s: dst_head0 + n_loc exceeds the destination pool's heads", W);
+    if (push->write_local != 0 && push->write_local != 1)
+      return fail(DS_ERR_INVALID_ARG, "%s: write_local must be 0 or 1", W);
+  }
   if (num_seqs == 0) return DS_OK;
-  if (!q || !k || !v || !out || !cu_seqlens || !block_table)
+  if (!q || !k || !v || !out || !cu_seqlens || !block_table || (push && !push->block_table))
     return fail(DS_ERR_INVALID_ARG, "%s: NULL pointer argument", W);
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out))
     return fail(DS_ERR_INVALID_ARG, "%s: q/k/v/out must be 16-B aligned", W);
   if (total_tokens < num_seqs || max_seqlen < 1 || max_seqlen > total_tokens)
     return fail(DS_ERR_INVALID_ARG, "%s: need num_seqs <= total_tokens and 1 <= max_seqlen <= total_tokens", W);
   if (layer < 0 || layer >= cache->num_layers) return fail(DS_ERR_INVALID_ARG, "%s: layer out of range", W);
-  if ((max_seqlen + 15) / 16 > max_blocks_per_seq)
+  if ((max_seqlen + 15) / 16 > max_blocks_per_seq || (push && (max_seqlen + 15) / 16 > push->max_blocks))
     return fail(DS_ERR_INVALID_ARG, "%s: max_seqlen needs more than max_blocks_per_seq pages", W);
   if (!(softmax_scale > 0.f) || !isfinite(softmax_scale))
     return fail(DS_ERR_INVALID_ARG, "%s: softmax_scale must be finite and > 0", W);
@@ -164,14 +181,16 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
   // at every length, profiles/r01). DS_PREFILL_KERNEL=2q selects the experimental
   // ping-pong pair-of-q-tiles CTA (prefill2q.cu; parity-tested, slower today).
   static const char *force = getenv("DS_PREFILL_KERNEL");
-  const bool two_q = force && strcmp(force, "2q") == 0;
+  const bool two_q = force && strcmp(force, "2q") == 0 && !push;
   const int kv_rows = two_q ? 128 : kPrefillKVRows;
-  CUtensorMap tq, tk, tv, tc, to;
+  CUtensorMap tq, tk, tv, tc, to, tdst;
   if (ds_status s = qkv_map(&tq, q, total_tokens, n, D, kPrefillQRows, W)) return s;
   if (ds_status s = out_map(&to, out, total_tokens, n, D, W)) return s;
   if (ds_status s = qkv_map(&tk, k, total_tokens, n, D, kv_rows, W)) return s;
   if (ds_status s = qkv_map(&tv, v, total_tokens, n, D, kv_rows, W)) return s;
   if (ds_status s = cache_map(&tc, cache, W)) return s;
+  if (push)
+    if (ds_status s = cache_map(&tdst, push->cache, W)) return s;
   PrefillArgs a{};
   a.out = out;
   a.cu_seqlens = cu_seqlens;
@@ -186,10 +205,43 @@ extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v
   a.layer = layer;
   a.num_blocks = cache->num_blocks;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
+  a.write_local = 1;
+  if (push) {
+    a.dst_block_table = push->block_table;
+    a.dst_max_blocks = push->max_blocks;
+    a.dst_layer = push->layer;
+    a.dst_num_blocks = push->cache->num_blocks;
+    a.dst_head0 = push->head0;
+    a.write_local = push->write_local;
+  }
   cudaError_t e = two_q ? launch_prefill2q(a, tq, tk, tv, tc, to, D, static_cast<cudaStream_t>(stream))
-                        : launch_prefill(a, tq, tk, tv, tc, to, D, static_cast<cudaStream_t>(stream));
+                        : launch_prefill(a, tq, tk, tv, tc, to, push ? &tdst : nullptr, D,
+                                         static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, W);
   return DS_OK;
+}
+
+extern "C" ds_status ds_prefill_attn(const void *q, const void *k, const void *v, void *out,
+                                     const int32_t *cu_seqlens, int32_t num_seqs,
+                                     int32_t total_tokens, int32_t max_seqlen,
+                                     const ds_kv_cache *cache, int32_t layer,
+                                     const int32_t *block_table, int32_t max_blocks_per_seq,
+                                     float softmax_scale, void *stream) {
+  return prefill_impl("ds_prefill_attn", q, k, v, out, cu_seqlens, num_seqs, total_tokens, max_seqlen, cache, layer,
+                      block_table, max_blocks_per_seq, softmax_scale, nullptr, stream);
+}
+
+extern "C" ds_status ds_prefill_attn_push(const void *q, const void *k, const void *v, void *out,
+                                          const int32_t *cu_seqlens, int32_t num_seqs, int32_t total_tokens,
+                                          int32_t max_seqlen, const ds_kv_cache *cache, int32_t layer,
+                                          const int32_t *block_table, int32_t max_blocks_per_seq,
+                                          const ds_kv_cache *dst_cache, int32_t dst_layer,
+                                          const int32_t *dst_block_table, int32_t dst_max_blocks_per_seq,
+                                          int32_t dst_head0, int32_t write_local, float softmax_scale,
+                                          void *stream) {
+  const PushTarget push{dst_cache, dst_layer, dst_block_table, dst_max_blocks_per_seq, dst_head0, write_local};
+  return prefill_impl("ds_prefill_attn_push", q, k, v, out, cu_seqlens, num_seqs, total_tokens, max_seqlen, cache,
+                      layer, block_table, max_blocks_per_seq, softmax_scale, &push, stream);
 }
 
 extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const void *v, void *out,
@@ -236,7 +288,7 @@ extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const
   a.num_blocks = cache->num_blocks;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = launch_prefill(a, tq, tk, tv, tc, to, D, st);  // reads the prefix pages + the chunk
+  cudaError_t e = launch_prefill(a, tq, tk, tv, tc, to, nullptr, D, st);  // reads the prefix pages + the chunk
   if (e != cudaSuccess) return cuda_fail(e, W);
   KvAppendArgs ap{};  // then the chunk's K/V join the pages (positions prefix + t)
   ap.k = static_cast<const uint16_t *>(k);

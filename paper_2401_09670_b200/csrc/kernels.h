@@ -67,10 +67,15 @@ struct PrefillArgs {
   int32_t layer, num_blocks;   // cache layer / pool pages
   float scale_log2;
   int32_t persistent;          // CTAs take over unlaunched CTAs' items (cluster launch control)
+  // fused push migration (ds_prefill_attn_push): every page also goes to the
+  // destination pool (tm_dst) at dst_layer / dst_block_table / dst_head0
+  const int32_t *dst_block_table;  // [B][dst_max_blocks] or nullptr (no push)
+  int32_t dst_max_blocks, dst_layer, dst_num_blocks, dst_head0;
+  int32_t write_local;             // also write the source pool (tm_cache)
 };
 cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
                            const CUtensorMap &tm_v, const CUtensorMap &tm_cache, const CUtensorMap &tm_o,
-                           int head_dim, cudaStream_t stream);
+                           const CUtensorMap *tm_dst, int head_dim, cudaStream_t stream);
 size_t prefill_smem_bytes(int head_dim);
 int prefill_band_groups(int max_kv_len, int head_dim);  // L2-sized band of (sequence, head) groups
 bool prefill_persistent(int max_len);  // run the prefill CTAs persistently for this length?

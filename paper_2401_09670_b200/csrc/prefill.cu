@@ -156,11 +156,15 @@ DS_DEVICE void ctl_wait(uint64_t *bar, uint32_t parity) {
     mbar_wait(bar, parity);
 }
 
-template <int D, bool kChunked>
+// kPush: the fused push migration — every K/V page the kernel writes also goes,
+// from the same smem tile, to the destination pool (a peer GPU's pool mapped
+// through CUDA IPC, or another pool of this GPU) with a second TMA tensor store.
+template <int D, bool kChunked, bool kPush>
 __global__ void __launch_bounds__(kThreads, 2)
     prefill_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
                    const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_cache,
-                   const __grid_constant__ CUtensorMap tm_o, const PrefillArgs a) {
+                   const __grid_constant__ CUtensorMap tm_o, const __grid_constant__ CUtensorMap tm_dst,
+                   const PrefillArgs a) {
   using S = Smem<D>;
   constexpr int kChunks = D / 64;
 
@@ -194,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     tma_prefetch_desc(&tm_v);
     tma_prefetch_desc(&tm_cache);
     tma_prefetch_desc(&tm_o);
+    if (kPush) tma_prefetch_desc(&tm_dst);
   }
 
   int item = blockIdx.x;  // current item (linear launch index, see item_coords)
@@ -298,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           // chunk need not start on a page boundary)
           const int npg = kChunked ? 0 : min(8, (len - i * kBM + 15) >> 4);
           const int32_t *bt = btr + i * 8;
+          const int32_t *dbt = kPush ? a.dst_block_table + (size_t)r * a.dst_max_blocks + i * 8 : nullptr;
           for (int t = npt + 2 * i; npg > 0 && t < ntiles; ++t) {
             const uint32_t g = g0 + t;
             const int st = g & 1;
@@ -305,13 +311,19 @@ __global__ void __launch_bounds__(kThreads, 2)
             ctl_wait(&bars[B_VF + st], (g >> 1) & 1);
             for (int p = (t - npt - 2 * i) * 4; p < min(npg, (t - npt - 2 * i) * 4 + 4); ++p) {
               const int blk = bt[p];
+              const int dblk = kPush ? dbt[p] : 0;
 #pragma unroll
               for (int kv = 0; kv < 2; ++kv)
 #pragma unroll
-                for (int c = 0; c < kChunks; ++c)
-                  tma_store_4d(&tm_cache,
-                               smem + (kv ? S::V0 : S::K0) + st * S::kKVTile + c * kChunkBytes64 + (p & 3) * 16 * 128,
-                               c * 64, 0, h, (a.layer * 2 + kv) * a.num_blocks + blk);
+                for (int c = 0; c < kChunks; ++c) {
+                  const uint8_t *src =
+                      smem + (kv ? S::V0 : S::K0) + st * S::kKVTile + c * kChunkBytes64 + (p & 3) * 16 * 128;
+                  if (!kPush || a.write_local)
+                    tma_store_4d(&tm_cache, src, c * 64, 0, h, (a.layer * 2 + kv) * a.num_blocks + blk);
+                  if (kPush)
+                    tma_store_4d(&tm_dst, src, c * 64, 0, a.dst_head0 + h,
+                                 (a.dst_layer * 2 + kv) * a.dst_num_blocks + dblk);
+                }
             }
           }
           if (npg > 0) {
@@ -590,21 +602,21 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
-template <int D, bool C>
+template <int D, bool C, bool P>
 static cudaError_t set_prefill_smem_once() {
-  static cudaError_t st = cudaFuncSetAttribute(prefill_kernel<D, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static cudaError_t st = cudaFuncSetAttribute(prefill_kernel<D, C, P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                (int)Smem<D>::ALLOC);
   return st;
 }
 
-template <int D, bool C>
+template <int D, bool C, bool P>
 static cudaError_t launch_one(const PrefillArgs &a, const CUtensorMap &tq, const CUtensorMap &tk,
                               const CUtensorMap &tv, const CUtensorMap &tc, const CUtensorMap &to,
-                              cudaStream_t stream) {
-  cudaError_t e = set_prefill_smem_once<D, C>();
+                              const CUtensorMap &tdst, cudaStream_t stream) {
+  cudaError_t e = set_prefill_smem_once<D, C, P>();
   if (e != cudaSuccess) return e;
-  prefill_kernel<D, C><<<a.num_q_tiles * a.n_loc * a.num_seqs, kThreads, Smem<D>::ALLOC, stream>>>(tq, tk, tv, tc, to,
-                                                                                                  a);
+  prefill_kernel<D, C, P><<<a.num_q_tiles * a.n_loc * a.num_seqs, kThreads, Smem<D>::ALLOC, stream>>>(
+      tq, tk, tv, tc, to, tdst, a);
   return cudaGetLastError();
 }
 
@@ -660,13 +672,18 @@ size_t prefill_smem_bytes(int head_dim) {
 
 cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,
                            const CUtensorMap &tm_v, const CUtensorMap &tm_cache, const CUtensorMap &tm_o,
-                           int head_dim, cudaStream_t stream) {
+                           const CUtensorMap *tm_dst, int head_dim, cudaStream_t stream) {
   const bool chunked = a.prefix_lens != nullptr;
+  if (tm_dst) {  // fused push (regular prefill only)
+    if (chunked) return cudaErrorInvalidValue;
+    return head_dim == 128 ? launch_one<128, false, true>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, *tm_dst, stream)
+                           : launch_one<64, false, true>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, *tm_dst, stream);
+  }
   if (head_dim == 128)
-    return chunked ? launch_one<128, true>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, stream)
-                   : launch_one<128, false>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, stream);
-  return chunked ? launch_one<64, true>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, stream)
-                 : launch_one<64, false>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, stream);
+    return chunked ? launch_one<128, true, false>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, tm_o, stream)
+                   : launch_one<128, false, false>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, tm_o, stream);
+  return chunked ? launch_one<64, true, false>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, tm_o, stream)
+                 : launch_one<64, false, false>(a, tm_q, tm_k, tm_v, tm_cache, tm_o, tm_o, stream);
 }
 
 }  // namespace ds

@@ -148,6 +148,24 @@ def test_prefill_validation_then_no_device():
     assert "ds_prefill_attn" in ds.ds_last_error()
 
 
+def test_prefill_push_validation_then_no_device():
+    lib = ds.lib()
+    c = _cache(n=4)
+
+    def call(dst, dst_layer=0, head0=0, wl=1, dbt=FAKE, dmaxb=4):
+        return lib.ds_prefill_attn_push(FAKE, FAKE, FAKE, FAKE, FAKE, 2, 40, 33, ctypes.byref(c), 1, FAKE, 4,
+                                        ctypes.byref(dst), dst_layer, dbt, dmaxb, head0, wl, 0.125, None)
+    assert call(_cache(n=8, D=128)) == ds.DS_ERR_INVALID_ARG           # head_dim differs
+    assert call(_cache(n=8), dst_layer=2) == ds.DS_ERR_INVALID_ARG     # dst layer out of range
+    assert call(_cache(n=8), head0=5) == ds.DS_ERR_INVALID_ARG         # 5 + 4 heads > 8
+    assert call(_cache(n=8), wl=2) == ds.DS_ERR_INVALID_ARG
+    assert call(_cache(n=8), dbt=None) == ds.DS_ERR_INVALID_ARG
+    assert call(_cache(n=8), dmaxb=2) == ds.DS_ERR_INVALID_ARG         # 33 tokens need 3 pages
+    rc = call(_cache(n=8), head0=4)
+    assert rc == ds.DS_ERR_CUDA, ds.ds_last_error()
+    assert "ds_prefill_attn_push" in ds.ds_last_error()
+
+
 def test_decode_validation_and_workspace():
     lib = ds.lib()
     c = _cache(n=4, D=128)

@@ -16,7 +16,7 @@ if not torch.cuda.is_available():
 
 import paper_2401_09670_b200 as ds  # noqa: E402
 import synthetic as syn  # noqa: E402
-from gpu_util import i32, pages_match, to_bits, to_dev, to_f64  # noqa: E402
+from gpu_util import i32, pages_match, to_bits, to_dev, to_f64, valid_slots  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 TOL = 2e-2
@@ -360,6 +360,51 @@ def test_migrate_local_bit_exact(oracle_mod):
     bits = to_bits(dst.cache.tensor)
     for layer in range(L):
         assert pages_match(bits, dst.opool, layer, lens, td)
+
+
+@pytest.mark.parametrize("d,write_local,dst_head0", [(64, True, 0), (128, False, 2), (128, True, 1)])
+def test_prefill_push_fused_migration(oracle_mod, d, write_local, dst_head0):
+    """a2-a6 fused (ds_prefill_attn_push): the prefill kernel stores every K/V page
+    into the destination (decoding) pool as well — at a different layer, with
+    different (fragmented) block ids and a head offset — and into its own pool only
+    if write_local. Destination pages must equal the oracle's migration of the
+    oracle's prefill pages, bit for bit; the attention output matches as usual."""
+    lens = [130, 45, 260, 17, 1]
+    n, L = 4, 3
+    b = syn.prefill_batch(31, lens, n, d)
+    src = Side(oracle_mod, L, 40, n, d)
+    dst = Side(oracle_mod, L, 60, n + 3, d, poison=True)
+    dst.fragment(8, 9)
+    maxb = _ceil(max(lens), BS)
+    tp, tpo = np.full((len(lens), maxb), -1, np.int32), np.full((len(lens), maxb), -1, np.int32)
+    td, tdo = tp.copy(), tpo.copy()
+    src.append([0] * len(lens), lens, tp, tpo)
+    dst.append([0] * len(lens), lens, td, tdo)
+    src_bits_before = to_bits(src.cache.tensor)
+    out = torch.empty((sum(lens), n, d), dtype=torch.bfloat16, device="cuda")
+    scale = 1.0 / math.sqrt(d)
+    layer, dst_layer = 1, 2
+    ds.ds_prefill_attn_push(to_dev(b.q), to_dev(b.k), to_dev(b.v), out, i32(b.cu_seqlens), max(lens), src.cache,
+                            layer, i32(tp), dst.cache, dst_layer, i32(td), scale, dst_head0=dst_head0,
+                            write_local=write_local)
+    torch.cuda.synchronize()
+    err = oracle_mod.max_rel_err(to_f64(out), oracle_mod.prefill(b.q, b.k, b.v, b.cu_seqlens, scale))
+    assert err <= TOL and err <= WARN_PREFILL, err
+    src.opool.write_prefill(layer, b.k, b.v, b.cu_seqlens, tpo)  # the oracle's a3 pages
+    bits = to_bits(dst.cache.tensor)
+    # every valid slot of destination page (dst_layer, kv, td[r][p], dst_head0 + h) equals
+    # the oracle's source page (layer, kv, tp[r][p], h): the migration's definition
+    for (r, blk, slot, t) in valid_slots(lens, tp):
+        dblk = td[r, t // BS]
+        for kv in (0, 1):
+            for h in range(n):
+                ref = src.opool.page(layer, kv, int(blk), h)[slot]
+                assert np.array_equal(bits[dst_layer, kv, dblk, dst_head0 + h, slot], ref), (r, t, kv, h)
+    src_bits = to_bits(src.cache.tensor)
+    if write_local:
+        assert pages_match(src_bits, src.opool, layer, lens, tp)
+    else:  # the source pool is untouched
+        assert np.array_equal(src_bits, src_bits_before)
 
 
 @pytest.mark.parametrize("mode", ["self", "local_side_stream"])
