@@ -81,6 +81,9 @@ def parse():
     p.add_argument("--e2e-trace", action="store_true", help="print a per-step copy/compute timeline to stderr")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graphs", action="store_true", help="eager decode launches (no CUDA graphs)")
+    p.add_argument("--no-fused-migration", action="store_true",
+                   help="N=1: prefill into the prefill pool, then a LOCAL page-copy migration (default: the "
+                        "prefill kernel stores the pages straight into the decode pool, ds_prefill_attn_push)")
     p.add_argument("--transport", default="nccl", choices=["nccl", "pull"],
                    help="N>1 KV migration: NCCL send/recv (default) or one-sided CUDA-IPC pull by the decoder")
     p.add_argument("--pg-backend", default="nccl", choices=["nccl", "gloo"],
@@ -211,7 +214,8 @@ def _i32(torch, a):
 class Engine:
     """Device state of one rank: pools, resident inputs, staging, CUDA graphs."""
 
-    def __init__(self, w: Workload, role, comm, seed, torch, ds, transport="nccl", stream_layers=False):
+    def __init__(self, w: Workload, role, comm, seed, torch, ds, transport="nccl", stream_layers=False,
+                 fused=False):
         self.w, self.role, self.comm, self.torch, self.ds = w, role, comm, torch, ds
         dev = "cuda"
         bf = torch.bfloat16
@@ -260,6 +264,9 @@ class Engine:
             self.graphs = None
         nblk = sum(w.pages)
         self.transport = "local" if role.phase == "both" else transport
+        # a2-a6 fused (ds_prefill_attn_push): with both instances on one GPU the prefill
+        # kernel writes the pages straight into the decode pool admitted for the batch
+        self.fused = fused and self.transport == "local" and not stream_layers
         # NEXT-2: migrate layer l as soon as its prefill is done, so the
         # transfer overlaps the prefill of the next layers (LOCAL: on a side stream;
         # NCCL: the library's own side stream). PULL stays whole-batch.
@@ -377,8 +384,12 @@ class Engine:
             i = layer % len(self.q)
             if self.layer_hook:
                 self.layer_hook("before", layer)
-            ds.ds_prefill_attn(self.q[i], self.k[i], self.v[i], self.out, self.cu, w.max_len, self.P, layer, tp_d,
-                               w.scale)
+            if self.fused:
+                ds.ds_prefill_attn_push(self.q[i], self.k[i], self.v[i], self.out, self.cu, w.max_len, self.P, layer,
+                                        tp_d, self.D, layer, self.td_dev, w.scale, write_local=False)
+            else:
+                ds.ds_prefill_attn(self.q[i], self.k[i], self.v[i], self.out, self.cu, w.max_len, self.P, layer,
+                                   tp_d, w.scale)
             if self.layer_hook:
                 self.layer_hook("after", layer)
             if self.stream_layers:
@@ -389,7 +400,7 @@ class Engine:
             self.pull_publish(peer, tp)
             self._mark(marks, "migrate")
             return
-        if not self.stream_layers:
+        if not self.stream_layers and not self.fused:
             self.migrate_layers(peer, src_ids, 0, w.L)
         if self.mig_stream is not None:
             self.torch.cuda.current_stream().wait_stream(self.mig_stream)
@@ -512,7 +523,8 @@ class Engine:
         ds, w = self.ds, self.w
         self.td = np.full((w.B, w.maxb), -1, np.int32)
         ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, [0] * w.B, w.lens, self.td)
-        self.dst_ids = self.page_ids(self.upload(self.td))
+        self.td_dev = self.upload(self.td)
+        self.dst_ids = self.page_ids(self.td_dev)
 
     def decode_batch(self, marks):
         """a1 (APPEND per step) + a7/a8 for `output` steps, then FREE"""
@@ -720,7 +732,8 @@ def run_ds(args):
         comm = ds.ds_comm_init(pairing.bootstrap_unique_id(ds.ds_comm_get_unique_id, rank, world, dist), world, rank)
     replicas = 1 if world == 1 else sum(1 for r in roles if r.phase == "decode") // (cfg["tp"] * cfg["pp"])
     eng = Engine(w, role, comm, seed=1234 + role.replica * 7919 + role.stage * 131 + role.tp_rank, torch=torch,
-                 ds=ds, transport=args.transport, stream_layers=args.stream_layers)
+                 ds=ds, transport=args.transport, stream_layers=args.stream_layers,
+                 fused=not args.no_fused_migration)
     if world > 1 and args.transport == "pull":
         import torch.distributed as dist
         ctl = dist.group.WORLD if args.pg_backend == "gloo" else dist.new_group(backend="gloo")
@@ -788,9 +801,14 @@ def run_ds(args):
     elif (role.phase != "decode" or world > 1) and not (args.transport == "pull" and role.phase == "prefill"):
         mig_ms = phase_ms("migrate") / nb  # (a pull prefill rank only publishes; its decoders move the bytes)
         comp["migrate_ms_per_batch"] = mig_ms
-        comp["kv_migrate_GBps"] = w.kv_payload_bytes() / (mig_ms / 1e3) / 1e9
-        comp["kv_migrate_page_GBps"] = w.kv_page_bytes() / (mig_ms / 1e3) / 1e9
-        comp["kv_migrate_path"] = ("LOCAL page copy (one GPU)" if world == 1 else
+        if eng.fused:  # no separate pass: the page bytes are part of the prefill kernel's writes
+            comp["kv_migrate_GBps"] = comp["kv_migrate_page_GBps"] = None
+        else:
+            comp["kv_migrate_GBps"] = w.kv_payload_bytes() / (mig_ms / 1e3) / 1e9
+            comp["kv_migrate_page_GBps"] = w.kv_page_bytes() / (mig_ms / 1e3) / 1e9
+        comp["kv_migrate_path"] = ("fused into the prefill kernel: pages stored straight into the decode pool "
+                                   "(ds_prefill_attn_push)" if eng.fused else
+                                   "LOCAL page copy (one GPU)" if world == 1 else
                                    "NCCL p2p over NVLink" if args.transport == "nccl" else
                                    "one-sided pull: decoder's kernel reads the IPC-mapped prefill pool")
         if world > 1:
