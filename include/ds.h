@@ -296,6 +296,20 @@ ds_status ds_kv_migrate(ds_comm comm, int32_t role, int32_t peer, const ds_kv_ca
                         int32_t dst_head_begin, int32_t dst_layer_begin, void *staging,
                         size_t staging_bytes, void *stream);
 
+/* a5 zero-copy: when a batch's pages are the consecutive ids [block_begin,
+ * block_begin + num_blocks) in the sender's pool and [dst_block_begin, ...) in
+ * the receiver's (fresh pools allocate that way: lowest free id first), and the
+ * migrated head range is the whole pool (same num_heads at both ends), each
+ * (layer, K|V) run is one contiguous region in both pools, so NCCL moves it pool
+ * to pool: no staging, no pack / unpack kernels. role SEND (cache = source) or
+ * RECV (cache = destination; block_begin = its first id; dst_* ignored) on the
+ * two ranks with identical counts, or SELF on one rank (cache -> dst_cache).
+ * Stream-ordered on `stream` (NCCL ops enqueued there). Errors as ds_kv_migrate. */
+ds_status ds_kv_migrate_contig(ds_comm comm, int32_t role, int32_t peer, const ds_kv_cache *cache,
+                               int32_t layer_begin, int32_t layer_count, int32_t block_begin,
+                               int32_t num_blocks, const ds_kv_cache *dst_cache,
+                               int32_t dst_block_begin, void *stream);
+
 /* ======================================================================
  * a5, one-sided pull: "decoding instances fetch KV cache
  * from prefill instances as needed, using the GPU memory of prefill instances

@@ -31,7 +31,7 @@ EXPORTED = (
     "ds_kv_staging_bytes", "ds_kv_pack", "ds_kv_unpack", "ds_comm_get_unique_id", "ds_comm_init",
     "ds_comm_destroy", "ds_kv_migrate_staging_bytes", "ds_kv_migrate", "ds_ipc_export_mem", "ds_ipc_open_mem",
     "ds_ipc_close_mem", "ds_event_create_ipc", "ds_event_open_ipc", "ds_event_record", "ds_event_wait",
-    "ds_event_destroy", "ds_prefill_attn_chunked", "ds_prefill_attn_push",
+    "ds_event_destroy", "ds_prefill_attn_chunked", "ds_prefill_attn_push", "ds_kv_migrate_contig",
 )
 
 
@@ -75,6 +75,7 @@ def _load():
         "ds_comm_init": ([P, i32, i32, ctypes.POINTER(P)], ctypes.c_int),
         "ds_comm_destroy": ([P], ctypes.c_int),
         "ds_kv_migrate_staging_bytes": ([cache_p, i32, i32, i32, i32], sz),
+        "ds_kv_migrate_contig": ([P, i32, i32, cache_p, i32, i32, i32, i32, cache_p, i32, P], ctypes.c_int),
         "ds_kv_migrate": ([P, i32, i32, cache_p, i32, i32, P, i32, i32, i32, cache_p, P, i32, i32, P, sz, P],
                           ctypes.c_int),
         "ds_ipc_export_mem": ([P, P, ctypes.POINTER(sz)], ctypes.c_int),
@@ -381,6 +382,24 @@ def ds_kv_migrate(comm: Comm | None, role: int, peer: int, cache, layer_begin: i
                               None if dst_cache is None else dst_cache.ref(), _ptr(dst_block_ids),
                               dst_head_begin, layer_begin if dst_layer_begin is None else dst_layer_begin,
                               _ptr(staging), 0 if staging is None else _nbytes(staging), _stream(stream)))
+
+
+def ds_kv_migrate_contig(comm: Comm, role: int, peer: int, cache, layer_begin: int, layer_count: int,
+                         block_begin: int, num_blocks: int, dst_cache: KVCache | None = None,
+                         dst_block_begin: int = 0, stream=None):
+    """a5 zero-copy: pages [block_begin, +num_blocks) of every layer move pool to pool
+    through NCCL (consecutive ids at both ends, all heads)."""
+    _check(_lib.ds_kv_migrate_contig(comm._h, role, peer, cache.ref(), layer_begin, layer_count, block_begin,
+                                     num_blocks, None if dst_cache is None else dst_cache.ref(), dst_block_begin,
+                                     _stream(stream)))
+
+
+def contiguous_run(ids) -> int | None:
+    """first id if `ids` (host, logical order) are consecutive, else None"""
+    a = np.asarray(ids).reshape(-1)
+    if a.size == 0 or not np.array_equal(a, np.arange(a[0], a[0] + a.size)):
+        return None
+    return int(a[0])
 
 
 # --------------------------------------------------------------------- a5, one-sided pull (CUDA IPC)

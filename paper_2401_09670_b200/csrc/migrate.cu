@@ -280,6 +280,61 @@ extern "C" ds_status ds_kv_migrate(ds_comm comm, int32_t role, int32_t peer,
   return DS_OK;
 }
 
+// a5 without a4 / a6: consecutive page ids on both ends and the whole head range
+// make every (layer, K|V) run of the batch one contiguous region of both pools,
+// so NCCL moves it pool to pool — no staging ring, no pack / unpack kernels (whose
+// HBM passes would compete with the prefill and decode kernels running beside the
+// transfer). One ncclGroup per layer (its K and V runs) on the caller's stream.
+extern "C" ds_status ds_kv_migrate_contig(ds_comm comm, int32_t role, int32_t peer, const ds_kv_cache *cache,
+                                          int32_t layer_begin, int32_t layer_count, int32_t block_begin,
+                                          int32_t num_blocks, const ds_kv_cache *dst_cache,
+                                          int32_t dst_block_begin, void *stream) {
+  const char *W = "ds_kv_migrate_contig";
+  if (!comm || !comm->comm) return fail(DS_ERR_STATE, "%s: invalid communicator", W);
+  if (role != DS_MIGRATE_SEND && role != DS_MIGRATE_RECV && role != DS_MIGRATE_SELF)
+    return fail(DS_ERR_INVALID_ARG, "%s: bad role (SEND, RECV or SELF)", W);
+  if (role == DS_MIGRATE_SELF) peer = comm->rank;
+  if (peer < 0 || peer >= comm->nranks) return fail(DS_ERR_INVALID_ARG, "%s: peer out of range", W);
+  if (role != DS_MIGRATE_SELF && peer == comm->rank)
+    return fail(DS_ERR_INVALID_ARG, "%s: SEND/RECV to self; use DS_MIGRATE_SELF", W);
+  if (!cache || (role == DS_MIGRATE_SELF && !dst_cache)) return fail(DS_ERR_INVALID_ARG, "%s: NULL cache", W);
+  if (layer_count < 0 || num_blocks < 0) return fail(DS_ERR_INVALID_ARG, "%s: negative count", W);
+  const ds_kv_cache *ends[2] = {cache, role == DS_MIGRATE_SELF ? dst_cache : cache};
+  const int32_t b0s[2] = {block_begin, role == DS_MIGRATE_SELF ? dst_block_begin : block_begin};
+  for (int e = 0; e < 2; ++e) {
+    const ds_kv_cache *c = ends[e];
+    if (!c->base || c->block_size != 16 || (c->head_dim != 64 && c->head_dim != 128))
+      return fail(DS_ERR_INVALID_ARG, "%s: bad cache descriptor", W);
+    if (layer_begin < 0 || layer_begin + layer_count > c->num_layers)
+      return fail(DS_ERR_INVALID_ARG, "%s: layer range outside the pool", W);
+    if (b0s[e] < 0 || (int64_t)b0s[e] + num_blocks > c->num_blocks)
+      return fail(DS_ERR_INVALID_ARG, "%s: block range outside the pool", W);
+  }
+  if (ends[1]->head_dim != cache->head_dim || ends[1]->num_heads != cache->num_heads)
+    return fail(DS_ERR_INVALID_ARG, "%s: source and destination geometry differ", W);
+  if ((int64_t)layer_count * num_blocks == 0) return DS_OK;
+  const int64_t blk_bytes = (int64_t)cache->num_heads * 16 * cache->head_dim * 2;
+  const size_t run = (size_t)(num_blocks * blk_bytes);
+  cudaStream_t A = static_cast<cudaStream_t>(stream);
+  for (int32_t l = layer_begin; l < layer_begin + layer_count; ++l) {
+    DS_NCCL(ncclGroupStart(), W);
+    for (int kv = 0; kv < 2; ++kv) {
+      if (role != DS_MIGRATE_RECV) {
+        const char *src = static_cast<const char *>(cache->base) +
+                          ((int64_t)(2 * l + kv) * cache->num_blocks + block_begin) * blk_bytes;
+        DS_NCCL(ncclSend(src, run, ncclUint8, peer, comm->comm, A), W);
+      }
+      if (role != DS_MIGRATE_SEND) {
+        const ds_kv_cache *d = ends[1];
+        char *dst = static_cast<char *>(d->base) + ((int64_t)(2 * l + kv) * d->num_blocks + b0s[1]) * blk_bytes;
+        DS_NCCL(ncclRecv(dst, run, ncclUint8, peer, comm->comm, A), W);
+      }
+    }
+    DS_NCCL(ncclGroupEnd(), W);
+  }
+  return DS_OK;
+}
+
 // ---------------------------------------------------------------- CUDA IPC (PULL)
 struct ds_event_s {
   cudaEvent_t ev = nullptr;

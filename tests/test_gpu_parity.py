@@ -334,6 +334,49 @@ def test_migrate_self_through_nccl(oracle_mod):
         assert pages_match(bits, dst.opool, layer, lens, td)
 
 
+def test_migrate_contig_zero_copy_through_nccl(oracle_mod):
+    """a5 zero-copy (ds_kv_migrate_contig, SELF on one rank): consecutive source
+    pages [3, 3+nb) and destination pages [5, 5+nb) of every layer move pool to
+    pool through NCCL, no staging; the destination's valid slots equal the oracle's
+    migrated pages and pages outside the run are untouched."""
+    lens = [40, 17, 33]
+    n, d, L = 4, 128, 2
+    b = syn.prefill_batch(41, lens, n, d)
+    src = Side(oracle_mod, L, 24, n, d)
+    dst = Side(oracle_mod, L, 24, n, d, poison=True)
+    pad = np.full((1, 4), -1, np.int32)
+    src.append([0], [48], pad.copy(), pad.copy())  # ids 0-2 taken: the batch starts at 3
+    d_pad, d_pad_o = np.full((1, 5), -1, np.int32), np.full((1, 5), -1, np.int32)
+    dst.append([0], [80], d_pad, d_pad_o)  # ids 0-4 taken: the destination run starts at 5
+    maxb = _ceil(max(lens), BS)
+    tp, tpo = np.full((3, maxb), -1, np.int32), np.full((3, maxb), -1, np.int32)
+    td, tdo = tp.copy(), tpo.copy()
+    src.append([0] * 3, lens, tp, tpo)
+    dst.append([0] * 3, lens, td, tdo)
+    sblk = np.concatenate([tp[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+    dblk = np.concatenate([td[i, :_ceil(l, BS)] for i, l in enumerate(lens)])
+    s0, d0 = ds.contiguous_run(sblk), ds.contiguous_run(dblk)
+    assert s0 == 3 and d0 == 5, (sblk, dblk)
+    out = torch.empty((sum(lens), n, d), dtype=torch.bfloat16, device="cuda")
+    for layer in range(L):
+        ds.ds_prefill_attn(to_dev(b.q), to_dev(b.k), to_dev(b.v), out, i32(b.cu_seqlens), max(lens), src.cache,
+                           layer, i32(tp), 0.088)
+        src.opool.write_prefill(layer, b.k, b.v, b.cu_seqlens, tpo)
+    before = to_bits(dst.cache.tensor)
+    comm = ds.ds_comm_init(ds.ds_comm_get_unique_id(), 1, 0)
+    ds.ds_kv_migrate_contig(comm, ds.DS_MIGRATE_SELF, 0, src.cache, 0, L, s0, len(sblk), dst_cache=dst.cache,
+                            dst_block_begin=d0)
+    torch.cuda.synchronize()
+    comm.close()
+    oracle_mod.migrate(src.opool, dst.opool, 0, L, sblk, dblk, 0, 0, n)
+    bits = to_bits(dst.cache.tensor)
+    for layer in range(L):
+        assert pages_match(bits, dst.opool, layer, lens, td)
+    outside = np.ones(bits.shape[2], bool)
+    outside[d0:d0 + len(dblk)] = False
+    assert np.array_equal(bits[:, :, outside], before[:, :, outside])
+
+
 def test_migrate_local_bit_exact(oracle_mod):
     """LOCAL migration (both instances on one device): one page-copy kernel."""
     lens = [130, 7]
