@@ -81,6 +81,9 @@ def parse():
     p.add_argument("--e2e-trace", action="store_true", help="print a per-step copy/compute timeline to stderr")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-graphs", action="store_true", help="eager decode launches (no CUDA graphs)")
+    p.add_argument("--packed-migration", action="store_true",
+                   help="N>1 NCCL: pack -> send/recv -> unpack through staging (default: zero-copy pool-to-pool "
+                        "ds_kv_migrate_contig, the batch's pages being one run of ids at both ends)")
     p.add_argument("--no-fused-migration", action="store_true",
                    help="N=1: prefill into the prefill pool, then a LOCAL page-copy migration (default: the "
                         "prefill kernel stores the pages straight into the decode pool, ds_prefill_attn_push)")
@@ -215,7 +218,7 @@ class Engine:
     """Device state of one rank: pools, resident inputs, staging, CUDA graphs."""
 
     def __init__(self, w: Workload, role, comm, seed, torch, ds, transport="nccl", stream_layers=False,
-                 fused=False):
+                 fused=False, no_contig=False):
         self.w, self.role, self.comm, self.torch, self.ds = w, role, comm, torch, ds
         dev = "cuda"
         bf = torch.bfloat16
@@ -267,6 +270,8 @@ class Engine:
         # a2-a6 fused (ds_prefill_attn_push): with both instances on one GPU the prefill
         # kernel writes the pages straight into the decode pool admitted for the batch
         self.fused = fused and self.transport == "local" and not stream_layers
+        self.no_contig = no_contig
+        self.contig = None
         # NEXT-2: migrate layer l as soon as its prefill is done, so the
         # transfer overlaps the prefill of the next layers (LOCAL: on a side stream;
         # NCCL: the library's own side stream). PULL stays whole-batch.
@@ -379,6 +384,7 @@ class Engine:
         tp = np.full((w.B, w.maxb), -1, np.int32)
         ds.ds_block_table(self.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
         tp_d = self.upload(tp)
+        self.contig = self.contig_run(tp)
         src_ids = self.page_ids(tp_d)
         for layer in range(w.L):
             i = layer % len(self.q)
@@ -419,6 +425,9 @@ class Engine:
                 ds.ds_kv_migrate(None, self.mrole, 0, self.P, layer_begin, layer_count, src_ids, 0, w.n, None,
                                  dst_cache=self.D, dst_block_ids=self.dst_ids)
             self.launches += 1
+        elif self.contig is not None:  # zero-copy: the batch's pages are one run in both pools
+            ds.ds_kv_migrate_contig(self.comm, self.mrole, peer, self.P, layer_begin, layer_count, self.contig,
+                                    sum(w.pages))
         else:
             ds.ds_kv_migrate(self.comm, self.mrole, peer, self.P, layer_begin, layer_count, src_ids, 0, w.n,
                              self.staging)
@@ -509,14 +518,32 @@ class Engine:
             # the receiver posts the same per-layer (or whole-batch) calls as its sender
             per = [(l, 1) for l in range(w.L)] if self.stream_layers else [(0, w.L)]
             for l0, nl in per:
-                ds.ds_kv_migrate(self.comm, self.mrole, role.peer, self.D, l0, nl, self.dst_ids, 0, w.n, self.staging)
-                self.launches += self.migrate_chunks(nl)
+                if self.contig is not None:
+                    ds.ds_kv_migrate_contig(self.comm, self.mrole, role.peer, self.D, l0, nl, self.contig,
+                                            sum(w.pages))
+                else:
+                    ds.ds_kv_migrate(self.comm, self.mrole, role.peer, self.D, l0, nl, self.dst_ids, 0, w.n,
+                                     self.staging)
+                    self.launches += self.migrate_chunks(nl)
         self._mark(marks, "migrate")
 
     def migrate_chunks(self, layers):
         w = self.w
         chunk_rows = max(1, (64 << 20) // (w.n * 16 * w.d * 2))
         return -(-(2 * layers * sum(w.pages)) // chunk_rows)  # pack or unpack kernels (+ NCCL's own)
+
+    def contig_run(self, table):
+        """NCCL transport: first id if the batch's pages (logical order) are one run of
+        consecutive ids — always, since each pool holds one batch at a time and hands
+        out the lowest free ids — so the zero-copy ds_kv_migrate_contig applies; both
+        ends decide the same way (their pools are built alike), else None"""
+        if self.transport != "nccl" or self.no_contig:
+            return None
+        ids = np.concatenate([table[b, :p] for b, p in enumerate(self.w.pages)])
+        run = self.ds.contiguous_run(ids)
+        if run is None:
+            raise RuntimeError("batch pages are not one run: the zero-copy migration would mismatch its peer")
+        return run
 
     def admit(self):
         """decode-side admission of one batch (pull): pages for the prompts"""
@@ -525,6 +552,7 @@ class Engine:
         ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, [0] * w.B, w.lens, self.td)
         self.td_dev = self.upload(self.td)
         self.dst_ids = self.page_ids(self.td_dev)
+        self.contig = self.contig_run(self.td)
 
     def decode_batch(self, marks):
         """a1 (APPEND per step) + a7/a8 for `output` steps, then FREE"""
@@ -733,7 +761,7 @@ def run_ds(args):
     replicas = 1 if world == 1 else sum(1 for r in roles if r.phase == "decode") // (cfg["tp"] * cfg["pp"])
     eng = Engine(w, role, comm, seed=1234 + role.replica * 7919 + role.stage * 131 + role.tp_rank, torch=torch,
                  ds=ds, transport=args.transport, stream_layers=args.stream_layers,
-                 fused=not args.no_fused_migration)
+                 fused=not args.no_fused_migration, no_contig=args.packed_migration)
     if world > 1 and args.transport == "pull":
         import torch.distributed as dist
         ctl = dist.group.WORLD if args.pg_backend == "gloo" else dist.new_group(backend="gloo")
@@ -809,7 +837,9 @@ def run_ds(args):
         comp["kv_migrate_path"] = ("fused into the prefill kernel: pages stored straight into the decode pool "
                                    "(ds_prefill_attn_push)" if eng.fused else
                                    "LOCAL page copy (one GPU)" if world == 1 else
-                                   "NCCL p2p over NVLink" if args.transport == "nccl" else
+                                   ("NCCL p2p over NVLink, pool to pool (zero-copy)" if eng.contig is not None
+                                    else "NCCL p2p over NVLink (pack / unpack via staging)")
+                                   if args.transport == "nccl" else
                                    "one-sided pull: decoder's kernel reads the IPC-mapped prefill pool")
         if world > 1:
             comp["kv_migrate_frac_of_nvlink"] = comp["kv_migrate_page_GBps"] / NVLINK_GBS

@@ -215,3 +215,12 @@ def test_pack_validation():
     assert lib.ds_kv_pack(ctypes.byref(c), 0, 2, FAKE, 3, 2, 3, FAKE, 1 << 20, None) == ds.DS_ERR_INVALID_ARG
     assert lib.ds_kv_pack(ctypes.byref(c), 0, 2, FAKE, 3, 0, 4, FAKE, 100, None) == ds.DS_ERR_INVALID_ARG
     assert lib.ds_kv_pack(ctypes.byref(c), 0, 2, FAKE, 3, 0, 4, FAKE, 1 << 20, None) == ds.DS_ERR_CUDA
+
+
+def test_contiguous_run_helper():
+    """the host check that picks the zero-copy migration (ds_kv_migrate_contig)"""
+    assert ds.contiguous_run([3, 4, 5, 6]) == 3
+    assert ds.contiguous_run(np.array([[0, 1], [2, 3]])) == 0
+    assert ds.contiguous_run([3, 5]) is None
+    assert ds.contiguous_run([4, 3]) is None
+    assert ds.contiguous_run([]) is None
