@@ -147,6 +147,56 @@ def test_prefill_full_size_config2_sampled(oracle_mod):
     assert not np.isnan(got).any()
 
 
+def test_bench_step_shape_fused_prefill_then_dynamic_decode(oracle_mod):
+    """The bench's default launch configuration (config 2: OPT-13B heads, 128 x 512-token
+    prompts): the fused prefill+migration into the decode pool (sampled output rows vs
+    the oracle; every destination page slot vs the input K/V bits, the plain definition
+    of the migrated cache), then one decode step over all 128 x 40 pairs, which runs
+    the dynamic-tail decode instance (>= 64 pages per warp), against the oracle."""
+    B, l, n, d = 128, 512, 40, 128
+    lens = [l] * B
+    b = syn.prefill_batch(51, lens, n, d)
+    nb = B * (l // BS + 1) + 8
+    src = Side(oracle_mod, 1, B * (l // BS) + 8, n, d)
+    dst = Side(oracle_mod, 1, nb, n, d, poison=True)
+    tp, tpo = np.full((B, l // BS + 1), -1, np.int32), np.full((B, l // BS + 1), -1, np.int32)
+    td, tdo = tp.copy(), tpo.copy()
+    src.append([0] * B, lens, tp, tpo)
+    dst.append([0] * B, lens, td, tdo)
+    out = torch.empty((B * l, n, d), dtype=torch.bfloat16, device="cuda")
+    scale = 1.0 / math.sqrt(d)
+    ds.ds_prefill_attn_push(to_dev(b.q), to_dev(b.k), to_dev(b.v), out, i32(b.cu_seqlens), l, src.cache, 0, i32(tp),
+                            dst.cache, 0, i32(td), scale, write_local=False)
+    torch.cuda.synchronize()
+    got = to_f64(out)
+    g = syn.rng(52)
+    err = 0.0
+    for r, i, h in [(int(g.integers(B)), int(g.integers(l)), int(g.integers(n))) for _ in range(24)] + \
+            [(0, 0, 0), (B - 1, l - 1, n - 1), (5, 127, 3), (77, 128, 39)]:
+        ref = oracle_mod.prefill_row(b.q, b.k, b.v, b.cu_seqlens, r, i, h, scale)
+        err = max(err, oracle_mod.max_rel_err(got[b.cu_seqlens[r] + i, h], ref))
+    assert err <= TOL and err <= WARN_PREFILL, err
+    bits = to_bits(dst.cache.tensor)  # [1][2][nb][n][16][d]
+    for r in range(B):
+        base = b.cu_seqlens[r]
+        for kv, src_bits in ((0, b.k), (1, b.v)):
+            want = src_bits[base:base + l].reshape(l // BS, BS, n, d).transpose(0, 2, 1, 3)  # [page][n][16][d]
+            assert np.array_equal(bits[0, kv, td[r, :l // BS]], want), (r, kv)
+    # one decode step at c = 512 (a new page per sequence) through the dynamic-tail instance
+    dst.opool.write_prefill(0, b.k, b.v, b.cu_seqlens, tdo)
+    cur = [l] * B
+    dst.append(cur, [1] * B, td, tdo)
+    db = syn.decode_batch(53, B, n, d)
+    o = torch.full((B, n, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    ws = torch.zeros(ds.ds_decode_workspace_bytes(B, n, d, l), dtype=torch.uint8, device="cuda")
+    ds.ds_decode_attn(to_dev(db.q), to_dev(db.k_new), to_dev(db.v_new), o, dst.cache, 0, i32(td), i32(cur), l, scale,
+                      ws)
+    torch.cuda.synchronize()
+    ref = dst.opool.decode(0, db.q, db.k_new, db.v_new, tdo, cur, scale)
+    derr = oracle_mod.max_rel_err(to_f64(o), ref)
+    assert derr <= WARN, derr
+
+
 # ------------------------------------------------------------------ a7 + a8
 def run_decode(oracle_mod, ctx, n, d, seed=0, steps=1, fragment=0, q_sigma=1.0, max_cache_len=None,
                table_cols=0, poison=False):
