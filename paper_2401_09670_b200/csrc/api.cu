@@ -201,7 +201,7 @@ static ds_status prefill_impl(const char *W, const void *q, const void *k, const
   a.max_blocks = max_blocks_per_seq;
   a.num_q_tiles = two_q ? (max_seqlen + 255) / 256 : (max_seqlen + 127) / 128;
   a.persistent = prefill_persistent(max_seqlen);
-  a.band_groups = prefill_band_groups(max_seqlen, D);
+  prefill_set_grid(a, total_tokens);
   a.layer = layer;
   a.num_blocks = cache->num_blocks;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;
@@ -283,7 +283,7 @@ extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const
   a.max_blocks = max_blocks_per_seq;
   a.num_q_tiles = (max_chunk_len + 127) / 128;
   a.persistent = prefill_persistent(max_context_len);  // an item attends the prefix + its chunk rows
-  a.band_groups = prefill_band_groups(max_context_len, D);
+  prefill_set_grid(a, total_tokens);
   a.layer = layer;
   a.num_blocks = cache->num_blocks;
   a.scale_log2 = softmax_scale * 1.4426950408889634f;

@@ -63,7 +63,8 @@ struct PrefillArgs {
   const int32_t *prefix_lens;  // [B] cached tokens before the chunk (chunked prefill) or nullptr
   const int32_t *block_table;  // [B][max_blocks]
   int32_t num_seqs, n_loc, max_blocks, num_q_tiles;
-  int32_t band_groups;         // (sequence, head) groups per scheduling band (prefill_band_groups)
+  int32_t compact;             // item space = existing q tiles only (num_seqs <= kPrefillCompactSeqs)
+  int64_t grid_items;          // launched items (CTAs before work stealing)
   int32_t layer, num_blocks;   // cache layer / pool pages
   float scale_log2;
   int32_t persistent;          // CTAs take over unlaunched CTAs' items (cluster launch control)
@@ -77,7 +78,10 @@ cudaError_t launch_prefill(const PrefillArgs &a, const CUtensorMap &tm_q, const 
                            const CUtensorMap &tm_v, const CUtensorMap &tm_cache, const CUtensorMap &tm_o,
                            const CUtensorMap *tm_dst, int head_dim, cudaStream_t stream);
 size_t prefill_smem_bytes(int head_dim);
-int prefill_band_groups(int max_kv_len, int head_dim);  // L2-sized band of (sequence, head) groups
+constexpr int kPrefillCompactSeqs = 1024;  // sequences whose tile prefix fits the prefill CTA's smem
+// items to launch: compact = n_loc x an upper bound of sum ceil(len/128) from the
+// host-side token total; else num_q_tiles x n_loc x num_seqs
+void prefill_set_grid(PrefillArgs &a, int64_t total_tokens);
 bool prefill_persistent(int max_len);  // run the prefill CTAs persistently for this length?
 // experimental (DS_PREFILL_KERNEL=2q): two 128-row q tiles per CTA, 128-key tiles
 cudaError_t launch_prefill2q(const PrefillArgs &a, const CUtensorMap &tm_q, const CUtensorMap &tm_k,

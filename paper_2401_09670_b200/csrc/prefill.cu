@@ -38,6 +38,7 @@ namespace ds {
 namespace {
 
 constexpr int kBM = 128, kBN = 64;  // q rows per CTA, keys per kv tile
+constexpr int kCompactSeqs = kPrefillCompactSeqs;
 constexpr int kThreads = 192;
 constexpr uint32_t kChunkBytes128 = 128 * 128;  // Q: 128 rows x 128 B (64 bf16) per SW128 column block
 constexpr uint32_t kChunkBytes64 = 64 * 128;    // K/V tile: 64 rows x 128 B per SW128 column block
@@ -59,7 +60,8 @@ struct Smem {
   static constexpr uint32_t K0 = Q + kQTile;           // 2 stages
   static constexpr uint32_t V0 = K0 + 2 * kKVTile;     // 2 stages
   static constexpr uint32_t OST = V0 + 2 * kKVTile;    // epilogue staging: 4 warps x 32 rows x 32 dims bf16
-  static constexpr uint32_t CLC = OST + 4 * 2048;      // 2 x 16-B work-stealing responses
+  static constexpr uint32_t PREF = OST + 4 * 2048;     // int[kCompactSeqs + 1] tile prefix + 8 warp totals
+  static constexpr uint32_t CLC = PREF + (kCompactSeqs + 1 + 8) * 4 + 12;  // 2 x 16-B work-stealing responses
   static constexpr uint32_t BAR = CLC + 32;
   static constexpr uint32_t kBars = 21;
   static constexpr uint32_t TMEM_SLOT = BAR + kBars * 8;
@@ -122,30 +124,64 @@ enum { T_SM_WAIT_S = 1, T_SM_GOT_S, T_SM_P_DONE, T_MMA_S, T_MMA_WAIT_P, T_MMA_PV
        T_SM_EPI_PV, T_EPI_LD = 32 /* 32 + 2*chunk: TMEM chunk loaded; +1: chunk stored */,
        T_SM_WARP_P = 16 /* + warp (< 32) */ };
 
-// Launch order of the work items (q tile i, head h, sequence r). The G = n_loc x
-// num_seqs (sequence, head) groups are cut into bands of a.band_groups groups whose
-// K/V fit comfortably in L2; inside a band the items go heaviest q tile first
-// ACROSS the band's groups (global longest-processing-time order, so the last
-// items of the launch are the cheapest and the persistent CTAs finish together),
-// while the K/V re-reads of a group stay within its band's time window (L2 hits).
-// band_groups = 1 is the plain group-major order.
-DS_DEVICE void item_coords(const PrefillArgs &a, int item, int &i, int &h, int &r) {
-  const int Q = a.num_q_tiles, G = a.n_loc * a.num_seqs, Gb = a.band_groups;
-  const int full = G / Gb, per_band = Gb * Q;
-  int band, k, gsz;
-  if (item < full * per_band) {
-    band = item / per_band;
-    k = item - band * per_band;
-    gsz = Gb;
-  } else {
-    band = full;
-    k = item - full * per_band;
-    gsz = G - full * Gb;
+// Launch order of the work items (q tile i, head h, sequence r): sequences in order,
+// their heads in order, and the q tiles of one (sequence, head) adjacent, heaviest
+// first (their K/V re-reads hit L2). With a.compact the item space holds only the
+// tiles that exist: pref[r] = sum of ceil(len/128) over the sequences before r (built
+// in smem once per CTA), so a batch of mixed lengths launches no empty items — each
+// costs a persistent CTA ~0.5 us to skip (64 x 128-token prompts launched with a
+// 2048-token bound: 85 -> 144 us). Items past the last tile come back as i = -1.
+// Without it (num_seqs > kCompactSeqs) the grid is num_q_tiles x n_loc x num_seqs.
+DS_DEVICE void item_coords(const PrefillArgs &a, const int *pref, int item, int &i, int &h, int &r) {
+  if (!a.compact) {
+    const int Q = a.num_q_tiles, g = item / Q;
+    i = Q - 1 - (item - g * Q);
+    r = g / a.n_loc;
+    h = g - r * a.n_loc;
+    return;
   }
-  const int level = k / gsz, group = band * Gb + (k - level * gsz);
-  i = Q - 1 - level;
-  r = group / a.n_loc;
-  h = group - r * a.n_loc;
+  const int n = a.n_loc;
+  if (item >= n * pref[a.num_seqs]) {
+    i = -1;
+    r = h = 0;
+    return;
+  }
+  int lo = 0, hi = a.num_seqs - 1;  // largest r with n * pref[r] <= item
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (n * pref[mid] <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  r = lo;
+  const int tr = pref[r + 1] - pref[r], k = item - n * pref[r];
+  h = k / tr;
+  i = tr - 1 - (k - h * tr);
+}
+
+// pref[r] = sum_{r' < r} ceil(len_r' / 128), r in [0, num_seqs], by all threads of
+// the CTA (per-thread runs, warp shuffle scan, one pass over the warp totals)
+DS_DEVICE void build_tile_prefix(const PrefillArgs &a, int *pref, int *warp_tot) {
+  const int B = a.num_seqs, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int per = (B + kThreads - 1) / kThreads;
+  const int b0 = min(B, t * per), b1 = min(B, b0 + per);
+  int sum = 0;
+  for (int b = b0; b < b1; ++b) sum += (a.cu_seqlens[b + 1] - a.cu_seqlens[b] + kBM - 1) / kBM;
+  int inc = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  int base = 0;
+  for (int w = 0; w < warp; ++w) base += warp_tot[w];
+  int run = base + inc - sum;
+  for (int b = b0; b < b1; ++b) {
+    pref[b] = run;
+    run += (a.cu_seqlens[b + 1] - a.cu_seqlens[b] + kBM - 1) / kBM;
+  }
+  if (t == kThreads - 1) pref[B] = base + inc;
 }
 
 // waits of the producer and MMA threads
@@ -187,6 +223,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     tmem_alloc<kTmemCols>(tmem_slot);
     tmem_relinquish();
   }
+  int *pref = reinterpret_cast<int *>(smem + S::PREF);
+  if (a.compact) build_tile_prefix(a, pref, pref + kCompactSeqs + 1);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -229,10 +267,10 @@ __global__ void __launch_bounds__(kThreads, 2)
       clc_try_cancel(sbase + S::CLC + (q & 1) * 16, &bars[B_CLC + (q & 1)]);
     }
     int i, h, r;
-    item_coords(a, item, i, h, r);
+    item_coords(a, pref, item, i, h, r);
     const int seq_start = a.cu_seqlens[r];
     const int len = a.cu_seqlens[r + 1] - seq_start;
-    if (i * kBM < len) {
+    if (i >= 0 && i * kBM < len) {
       // chunked prefill (NEXT-3): the sequence already holds c0 tokens in the paged
       // cache; kv tiles [0, npt) are that prefix (read from the pages), tiles
       // [npt, ntiles) are the chunk's own keys 0 .. 2i+1 (64 keys each; the second
@@ -615,7 +653,7 @@ static cudaError_t launch_one(const PrefillArgs &a, const CUtensorMap &tq, const
                               const CUtensorMap &tdst, cudaStream_t stream) {
   cudaError_t e = set_prefill_smem_once<D, C, P>();
   if (e != cudaSuccess) return e;
-  prefill_kernel<D, C, P><<<a.num_q_tiles * a.n_loc * a.num_seqs, kThreads, Smem<D>::ALLOC, stream>>>(
+  prefill_kernel<D, C, P><<<(unsigned)a.grid_items, kThreads, Smem<D>::ALLOC, stream>>>(
       tq, tk, tv, tc, to, tdst, a);
   return cudaGetLastError();
 }
@@ -641,19 +679,10 @@ extern "C" __attribute__((visibility("default"))) int ds_debug_prefill_trace(uns
 }
 #endif
 
-int prefill_band_groups(int max_kv_len, int head_dim) {
-  // bands of (sequence, head) groups whose K + V (max_kv_len x head_dim bf16 each)
-  // fit a DS_PREFILL_BAND_MB budget. Default 0 = one group per band, the plain
-  // group-major order: measured (tools/kernel_bench.py) as fast or faster than
-  // 8/32/64 MiB bands at every length (the tail of the launch is not where the
-  // time goes; the per-SM tensor/smem pipeline is).
-  static const long budget = [] {
-    const char *e = getenv("DS_PREFILL_BAND_MB");
-    return (e ? atol(e) : 0L) << 20;
-  }();
-  const long per_group = (long)max_kv_len * head_dim * 4;
-  const long g = budget / (per_group > 0 ? per_group : 1);
-  return g < 1 ? 1 : g > (1 << 20) ? (1 << 20) : (int)g;
+void prefill_set_grid(PrefillArgs &a, int64_t total_tokens) {
+  a.compact = a.num_seqs <= kCompactSeqs;
+  a.grid_items = a.compact ? (int64_t)a.n_loc * ((total_tokens + (int64_t)(kBM - 1) * a.num_seqs) / kBM)
+                           : (int64_t)a.num_q_tiles * a.n_loc * a.num_seqs;
 }
 
 bool prefill_persistent(int /*max_len*/) {

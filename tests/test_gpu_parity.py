@@ -784,19 +784,15 @@ def test_prefill_persistence_forced(force):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("band_mb", ["0", "1"])
-def test_prefill_band_orders(band_mb):
-    """Launch-order bands (prefill_band_groups): DS_PREFILL_BAND_MB=0 is the plain
-    group-major order (one (sequence, head) group per band); 1 MiB gives bands of a
-    few groups and a partial last band at every parity shape. The item decode must
-    cover every (q tile, head, sequence) exactly once in either order."""
-    import os
-    import subprocess
-    import sys
-    env = dict(os.environ, DS_PREFILL_BAND_MB=band_mb)
-    here = os.path.dirname(os.path.abspath(__file__))
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
-                        os.path.join(here, "test_gpu_parity.py"), "-k",
-                        "(prefill or chunked) and not experimental and not forced and not band"],
-                       env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+@pytest.mark.parametrize("B", [1100, 700])
+def test_prefill_item_space_compact_and_full(oracle_mod, B):
+    """Work items: up to 1024 sequences the grid holds only the q tiles that exist
+    (a per-CTA smem prefix of ceil(len/128) maps items to (sequence, head, tile));
+    beyond that it is the full num_q_tiles x heads x sequences space with empty items
+    skipped. Both on a ragged batch of short and long prompts, every row vs the oracle."""
+    g = syn.rng(61 + B)
+    lens = [int(x) for x in g.integers(1, 40, B)]
+    lens[::97] = [300] * len(lens[::97])
+    b, side, table, got, err = run_prefill(oracle_mod, lens, 2, 64, seed=62)
+    assert err <= TOL and err <= WARN_PREFILL, err
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, lens, table)
