@@ -1,6 +1,6 @@
 """Prefill on the BASELINE length mixes (kernel only): python tools/pf_mix_probe.py
 Prints us, TFLOP/s and fraction of the attainable roofline per mix; honours
-DS_PKG_ROOT and the kernel's env knobs (e.g. DS_PREFILL_BAND_MB)."""
+DS_PKG_ROOT and the kernel's env knobs (e.g. DS_PREFILL_PERSISTENT)."""
 import os
 import sys
 
