@@ -87,8 +87,9 @@ def parse():
     p.add_argument("--no-fused-migration", action="store_true",
                    help="N=1: prefill into the prefill pool, then a LOCAL page-copy migration (default: the "
                         "prefill kernel stores the pages straight into the decode pool, ds_prefill_attn_push)")
-    p.add_argument("--transport", default="nccl", choices=["nccl", "pull"],
-                   help="N>1 KV migration: NCCL send/recv (default) or one-sided CUDA-IPC pull by the decoder")
+    p.add_argument("--transport", default="nccl", choices=["nccl", "pull", "push"],
+                   help="N>1 KV migration: NCCL send/recv (default), one-sided CUDA-IPC pull by the decoder, or "
+                        "push: the prefill kernel stores the pages into the decoder's IPC-mapped pool (fused)")
     p.add_argument("--pg-backend", default="nccl", choices=["nccl", "gloo"],
                    help="torch.distributed backend for plumbing (gloo lets 2 ranks share one GPU for rehearsal)")
     p.add_argument("--prefill-instances", type=int, default=0,
@@ -230,6 +231,8 @@ class Engine:
         # the (stream-ordered) migration of batch k; the decode side admits k+1 after k ends
         nb_p = sum(w.pages) * (2 * len(role.peers) if (transport == "pull" and role.phase == "prefill") else 1) + 16
         nb_d = sum(-(-(l + w.out_len) // 16) for l in w.lens) + 16
+        if transport == "push" and role.phase == "decode":
+            nb_d = 2 * nb_d  # the batch being decoded + the next one, admitted ahead and pushed into
         if self.pf:
             self.P = ds.KVCache.empty(w.L, nb_p, w.n, w.d)
             self.pool_p = ds.Pool(nb_p)
@@ -379,6 +382,8 @@ class Engine:
     def prefill_and_send(self, peer, marks):
         """a1 + a2/a3 for one batch, then a4-a6 towards decode rank `peer`."""
         ds, w = self.ds, self.w
+        if self.transport == "push":
+            return self.push_batch(peer, marks)
         if self.transport == "pull":
             self.pull_reclaim(peer, keep=1)  # a pool slot for this batch
         tp = np.full((w.B, w.maxb), -1, np.int32)
@@ -494,9 +499,107 @@ class Engine:
             work.wait()
         self.pending = []
 
+    # -- fused push (CUDA IPC): the prefill kernel stores into the decoder's pool ----------
+    def push_setup(self, roles, ctl):
+        """Decoders export their pool and one 'free' event per slot; prefill ranks map
+        every peer's pool and export one 'ready' event per (decoder, slot)."""
+        import torch.distributed as dist
+        ds, w, role = self.ds, self.w, self.role
+        self.ctl = ctl
+        info = {"rank": role.rank}
+        if role.phase == "prefill":
+            self.ready = {p: [ds.IpcEvent() for _ in range(2)] for p in role.peers}
+            info.update(ready={p: [e.handle for e in evs] for p, evs in self.ready.items()})
+        else:
+            self.free = [ds.IpcEvent() for _ in range(2)]
+            h, off = ds.ds_ipc_export_mem(self.D.tensor)
+            info.update(pool=(h, off, self.D.num_blocks), free=[e.handle for e in self.free])
+        self.pending = []
+        allinfo = [None] * role.world
+        dist.all_gather_object(allinfo, info, group=ctl)
+        if role.phase == "prefill":
+            self.remotes = {p: ds.RemoteKVCache(*allinfo[p]["pool"][:2], w.L, allinfo[p]["pool"][2], w.n, w.d)
+                            for p in role.peers}
+            self.peer_free = {p: [ds.IpcEvent(hd) for hd in allinfo[p]["free"]] for p in role.peers}
+        else:
+            self.peer_ready = [ds.IpcEvent(hd) for hd in allinfo[role.peer]["ready"][role.rank]]
+            self.announced = []  # host tables of admitted batches, in order
+            self.recvd = 0
+
+    def push_announce(self):
+        """decoder: admit the next batch (pages for its prompts) and send the table to
+        the prefill rank, which pushes the pages straight into them"""
+        torch, ds, w = self.torch, self.ds, self.w
+        td = np.full((w.B, w.maxb), -1, np.int32)
+        ds.ds_block_table(self.pool_d, ds.DS_BT_APPEND, [0] * w.B, w.lens, td)
+        k = self.recvd + len(self.announced)
+        msg = torch.from_numpy(np.concatenate([[k], td.reshape(-1)]).astype(np.int32))
+        self.pending.append((torch.distributed.isend(msg, self.role.peer, group=self.ctl), msg))
+        self.announced.append(td)
+
+    def push_batch(self, peer, marks):
+        """prefill rank: receive the decoder's table of batch k, then prefill with the
+        page stores going into its pool (ds_prefill_attn_push, write_local = 0)"""
+        ds, w, torch = self.ds, self.w, self.torch
+        msg = torch.zeros(1 + w.B * w.maxb, dtype=torch.int32)
+        torch.distributed.recv(msg, peer, group=self.ctl)
+        k = int(msg[0])
+        td = msg[1:].numpy().reshape(w.B, w.maxb)
+        tp = np.full((w.B, w.maxb), -1, np.int32)
+        ds.ds_block_table(self.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
+        tp_d, td_d = self.upload(tp), self.upload(td)
+        if k >= 2:
+            self.peer_free[peer][k % 2].wait()  # batch k-2 (same pages' slot parity) has been decoded
+        for layer in range(w.L):
+            i = layer % len(self.q)
+            if self.layer_hook:
+                self.layer_hook("before", layer)
+            ds.ds_prefill_attn_push(self.q[i], self.k[i], self.v[i], self.out, self.cu, w.max_len, self.P, layer,
+                                    tp_d, self.remotes[peer], layer, td_d, w.scale, write_local=False)
+            if self.layer_hook:
+                self.layer_hook("after", layer)
+        self.launches += w.L
+        self._mark(marks, "prefill")
+        self.ready[peer][k % 2].record()
+        note = torch.tensor([k], dtype=torch.int32)
+        self.pending.append((torch.distributed.isend(note, peer, group=self.ctl), note))
+        ds.ds_block_table(self.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
+        self._mark(marks, "migrate")
+
+    def push_drain(self):
+        """after the timed loop: every decoder announced one batch ahead; the prefill
+        ranks take those tables without pushing, decoders return the pages"""
+        if self.transport != "push":
+            return
+        torch, w = self.torch, self.w
+        if self.role.phase == "prefill":
+            for peer in self.role.peers:
+                msg = torch.zeros(1 + w.B * w.maxb, dtype=torch.int32)
+                torch.distributed.recv(msg, peer, group=self.ctl)
+        else:
+            for td in self.announced:
+                self.ds.ds_block_table(self.pool_d, self.ds.DS_BT_FREE, w.lens, None, td)
+            self.announced = []
+        for work, _ in self.pending:
+            work.wait()
+        self.pending = []
+
     def receive(self, marks):
         """decode rank: admit the batch, then migrate it in (NCCL recv, or PULL)"""
         ds, w, role, torch = self.ds, self.w, self.role, self.torch
+        if self.transport == "push":
+            if not self.announced:
+                self.push_announce()
+            self.push_announce()  # the next batch's pages, pushed while this one decodes
+            note = torch.zeros(1, dtype=torch.int32)
+            torch.distributed.recv(note, role.peer, group=self.ctl)
+            k = int(note[0])
+            assert k == self.recvd, (k, self.recvd)
+            self.peer_ready[k % 2].wait()  # the prefill kernels of batch k have stored its pages
+            self.td = self.announced.pop(0)
+            self.recvd = k + 1
+            self._mark(marks, "migrate")
+            return
         if self.transport == "pull":
             ids = torch.zeros(1 + w.B * max(w.pages), dtype=torch.int32)
             torch.distributed.recv(ids, role.peer, group=self.ctl)
@@ -596,6 +699,8 @@ class Engine:
         else:
             self.receive(marks)
             self.decode_batch(marks)
+            if self.transport == "push":
+                self.free[(self.recvd - 1) % 2].record()  # batch recvd-1's pages are read
 
 
 # ----------------------------------------------------------------------------- distributed
@@ -753,8 +858,8 @@ def run_ds(args):
     roles = roles_for(cfg, world, args)
     role = roles[rank]
     w = Workload(cfg, args, role)
-    if world == 1 or args.transport == "pull":
-        comm = None  # LOCAL page copy (one GPU) or CUDA-IPC pull: no NCCL communicator
+    if world == 1 or args.transport in ("pull", "push"):
+        comm = None  # one GPU (fused / LOCAL) or CUDA-IPC pull / push: no NCCL communicator
     else:
         import torch.distributed as dist
         comm = ds.ds_comm_init(pairing.bootstrap_unique_id(ds.ds_comm_get_unique_id, rank, world, dist), world, rank)
@@ -762,10 +867,10 @@ def run_ds(args):
     eng = Engine(w, role, comm, seed=1234 + role.replica * 7919 + role.stage * 131 + role.tp_rank, torch=torch,
                  ds=ds, transport=args.transport, stream_layers=args.stream_layers,
                  fused=not args.no_fused_migration, no_contig=args.packed_migration)
-    if world > 1 and args.transport == "pull":
+    if world > 1 and args.transport in ("pull", "push"):
         import torch.distributed as dist
         ctl = dist.group.WORLD if args.pg_backend == "gloo" else dist.new_group(backend="gloo")
-        eng.pull_setup(roles, ctl)
+        (eng.pull_setup if args.transport == "pull" else eng.push_setup)(roles, ctl)
     torch.cuda.synchronize()
     if args.profile:
         eng.step()
@@ -826,6 +931,9 @@ def run_ds(args):
         comp["migration"] = "streamed per layer (overlaps prefill)"
         comp["prefill_with_migration_ms_per_batch"] = pf_ms + phase_ms("migrate") / nb
         comp["migrate_tail_ms_per_batch"] = phase_ms("migrate") / nb
+    elif world > 1 and args.transport == "push":
+        comp["kv_migrate_path"] = ("fused into the prefill kernel: its page stores go into the decoder's "
+                                   "IPC-mapped pool over NVLink (ds_prefill_attn_push)")
     elif (role.phase != "decode" or world > 1) and not (args.transport == "pull" and role.phase == "prefill"):
         mig_ms = phase_ms("migrate") / nb  # (a pull prefill rank only publishes; its decoders move the bytes)
         comp["migrate_ms_per_batch"] = mig_ms
@@ -886,11 +994,13 @@ def run_ds(args):
             "config": _config_line(w, world, replicas, roles), "components": comp, "roofline": roofline,
             "clocks": clocks, "gpu_launches": eng.launches, "paper_context": paper}
     eng.pull_drain()
-    if world > 1:
+    eng.push_drain()
+    if world > 1 and args.transport != "push":  # push: the migration is inside the prefill kernel
         comp.update(measure_migration(eng, w, world, torch))
     if not args.no_e2e:
         line["e2e"] = run_e2e(args, eng, w, world, replicas, torch)
         eng.pull_drain()
+        eng.push_drain()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tok_s, threads, sample = oracle_sample_tok_s(w)
         line["cpu_baseline"] = {"value": tok_s, "unit": "tok/s", "cores": threads, "kind": "oracle",
