@@ -1048,6 +1048,7 @@ def measure_migration(eng, w, world, torch, reps=3):
             torch.distributed.recv(ids, role.peer, group=eng.ctl)
             tab = ids[1:].numpy().reshape(w.B, max(w.pages))
             pull_src = _i32(torch, np.concatenate([tab[b, :p] for b, p in enumerate(w.pages)]))
+    run = None if pull else eng.contig_run(tp if eng.pf else eng.td)
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -1059,7 +1060,12 @@ def measure_migration(eng, w, world, torch, reps=3):
                                  dst_cache=eng.D, dst_block_ids=eng.dst_ids)
         elif eng.pf:
             for peer in role.peers:
-                ds.ds_kv_migrate(eng.comm, eng.mrole, peer, eng.P, 0, w.L, src_ids, 0, w.n, eng.staging)
+                if run is not None:  # the step's default: zero-copy pool to pool
+                    ds.ds_kv_migrate_contig(eng.comm, eng.mrole, peer, eng.P, 0, w.L, run, sum(w.pages))
+                else:
+                    ds.ds_kv_migrate(eng.comm, eng.mrole, peer, eng.P, 0, w.L, src_ids, 0, w.n, eng.staging)
+        elif run is not None:
+            ds.ds_kv_migrate_contig(eng.comm, eng.mrole, role.peer, eng.D, 0, w.L, run, sum(w.pages))
         else:
             ds.ds_kv_migrate(eng.comm, eng.mrole, role.peer, eng.D, 0, w.L, eng.dst_ids, 0, w.n, eng.staging)
     e1.record()
