@@ -7,17 +7,19 @@ One STEP = one pass of the whole hot path over one batc
 of B synthetic requests:
   a1     block tables (prefill pool ALLOC/FREE; decode pool ALLOC/APPEND/FREE)
   a2+a3  ds_prefill_attn for every local layer (fused paged K/V write)
-  a4-a6  ds_kv_migrate of all local layers' pages, prefill pool -> decode pool
+  a4-a6  the pages of all local layers, prefill -> decode: at N=1 fused into the
+         prefill kernel (ds_prefill_attn_push into the decode pool); at N>1
+         ds_kv_migrate_contig (NCCL pool to pool), or pull / push over CUDA IPC
   a7+a8  `output` decode steps x local layers of ds_decode_attn
 Default workload = BASELINE configs[1] (config 2): OPT-13B attention geometry
 (40 layers x 40 heads x 128), 128 requests x 512 prompt / 64 output (the decode
 batch a dedicated decode instance accumulates — decoding is batched as far as
 memory allows, P:237; at N=1 both instances' pools, 2 x 56 GB, share the GPU;
 SURVEY §8d sweeps B = 1..256, profiles/r01/sweep_bench_c2_b*.json).
-At N=1 one GPU plays both instances (migration = LOCAL page copy); at N>1
+At N=1 one GPU plays both instances (migration fused into the prefill); at N>1
 ranks [0, N/2) are prefill and [N/2, N) decode instances, paired by
 paper_2401_09670_b200.pairing (same layers/heads), migration = NCCL
-p2p over NVLink; each replica pair serves its own batch (weak scaling) and the
+p2p over NVLink (pool to pool); each replica pair serves its own batch (weak scaling) and the
 prefill of batch k+1 overlaps the decode of batch k.
 
 value = (prompt + generated) tokens of all replicas / max-over-ranks step time.
