@@ -281,7 +281,7 @@ class Engine:
         # transfer overlaps the prefill of the next layers (LOCAL: on a side stream;
         # NCCL: the library's own side stream). PULL stays whole-batch.
         self.stream_layers = stream_layers and self.transport in ("local", "nccl")
-        self.mig_stream = torch.cuda.Stream() if (self.stream_layers and self.transport == "local") else None
+        self.mig_stream = torch.cuda.Stream() if (self.stream_layers and self.pf) else None
         self.mrole = {"local": ds.DS_MIGRATE_LOCAL, "pull": ds.DS_MIGRATE_PULL}.get(
             self.transport, ds.DS_MIGRATE_SEND if role.phase == "prefill" else ds.DS_MIGRATE_RECV)
         cache_for_size = self.P if self.pf else self.D
@@ -432,13 +432,20 @@ class Engine:
                 ds.ds_kv_migrate(None, self.mrole, 0, self.P, layer_begin, layer_count, src_ids, 0, w.n, None,
                                  dst_cache=self.D, dst_block_ids=self.dst_ids)
             self.launches += 1
-        elif self.contig is not None:  # zero-copy: the batch's pages are one run in both pools
-            ds.ds_kv_migrate_contig(self.comm, self.mrole, peer, self.P, layer_begin, layer_count, self.contig,
-                                    sum(w.pages))
         else:
-            ds.ds_kv_migrate(self.comm, self.mrole, peer, self.P, layer_begin, layer_count, src_ids, 0, w.n,
-                             self.staging)
-            self.launches += self.migrate_chunks(layer_count)
+            # streamed per layer: the sends run on a side stream, after this layer's
+            # prefill, while the main stream goes on with the next layers
+            st = self.mig_stream
+            if st is not None:
+                st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st if st is not None else torch.cuda.current_stream()):
+                if self.contig is not None:  # zero-copy: the batch's pages are one run in both pools
+                    ds.ds_kv_migrate_contig(self.comm, self.mrole, peer, self.P, layer_begin, layer_count,
+                                            self.contig, sum(w.pages))
+                else:
+                    ds.ds_kv_migrate(self.comm, self.mrole, peer, self.P, layer_begin, layer_count, src_ids, 0,
+                                     w.n, self.staging)
+                    self.launches += self.migrate_chunks(layer_count)
 
     # -- one-sided pull (CUDA IPC) ----------------------------------------------------
     def pull_setup(self, roles, ctl):
