@@ -360,8 +360,10 @@ class Engine:
         """ds_decode_attn for every local layer of decode step s (reads dtab / dlen)"""
         w, ds = self.w, self.ds
         for layer in range(w.L):
+            # layers > 0: the kernel just ahead is layer-1's decode, which writes none of
+            # layer's pages, the table or the lengths -> DS_DECODE_EARLY_KV is safe
             ds.ds_decode_attn(self.dq[s, layer], self.dk[s, layer], self.dv[s, layer], self.dout[s], self.D, layer,
-                              self.dtab[s], self.dlen[s], self.max_c, w.scale, self.ws)
+                              self.dtab[s], self.dlen[s], self.max_c, w.scale, self.ws, early_kv=layer > 0)
 
     def capture_decode_graphs(self):
         """one CUDA graph per decode step: the layer loop becomes a single launch"""

@@ -220,6 +220,28 @@ ds_status ds_decode_attn(const void *q, const void *k_new, const void *v_new, vo
                          float softmax_scale, void *workspace, size_t workspace_bytes,
                          void *stream);
 
+/* ds_decode_attn_ex — ds_decode_attn with a flags word (ds_decode_attn == flags 0).
+ * DS_DECODE_EARLY_KV: the kernel is launched with programmatic dependent launch
+ *   (PDL) and reads cache_lens, block_table and this layer's K/V pages BEFORE the
+ *   kernel ahead of it on the stream has finished (its first pages are already in
+ *   flight when that kernel drains); q, k_new, v_new, out and workspace are touched
+ *   only after it has finished. The CALLER guarantees that the immediately
+ *   preceding kernel on the stream writes neither cache_lens, nor block_table, nor
+ *   any page of `layer` that this call reads — e.g. a loop of ds_decode_attn over
+ *   the layers of one step (each call appends only to its own layer), or a kernel
+ *   that only produces q/k_new/v_new. (The kernel before that one has always
+ *   finished: an early call lets its successor start only after its own wait.)
+ *   A host copy ahead of the call is always safe (it ends the overlap). The
+ *   results are identical with and without the flag.
+ * Errors: as ds_decode_attn; DS_ERR_INVALID_ARG for unknown flag bits. */
+#define DS_DECODE_EARLY_KV 1u
+ds_status ds_decode_attn_ex(const void *q, const void *k_new, const void *v_new, void *out,
+                            const ds_kv_cache *cache, int32_t layer,
+                            const int32_t *block_table, int32_t max_blocks_per_seq,
+                            const int32_t *cache_lens, int32_t num_seqs, int32_t max_cache_len,
+                            float softmax_scale, void *workspace, size_t workspace_bytes,
+                            uint32_t flags, void *stream);
+
 /* ======================================================================
  * a4 / a6 — pack and unpack whole pages of a head slice (KV migration, P:363:
  * only between corresponding layers; P:633 head shards; reading R14: whole

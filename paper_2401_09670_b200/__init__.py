@@ -22,12 +22,13 @@ LIB_PATH = os.path.join(_PKG, "libds.so")
 DS_OK, DS_ERR_INVALID_ARG, DS_ERR_UNSUPPORTED, DS_ERR_NO_BLOCKS, DS_ERR_CUDA, DS_ERR_NCCL, DS_ERR_STATE = range(7)
 DS_BT_APPEND, DS_BT_FREE = 0, 1
 DS_MIGRATE_SEND, DS_MIGRATE_RECV, DS_MIGRATE_SELF, DS_MIGRATE_LOCAL, DS_MIGRATE_PULL = 0, 1, 2, 3, 4
+DS_DECODE_EARLY_KV = 1  # ds_decode_attn_ex flag
 BLOCK_SIZE = 16
 
 # every symbol include/ds.h declares (checked by tests/test_abi.py)
 EXPORTED = (
     "ds_last_error", "ds_build_info", "ds_pool_create", "ds_pool_destroy", "ds_pool_num_free",
-    "ds_block_table", "ds_prefill_attn", "ds_decode_workspace_bytes", "ds_decode_attn",
+    "ds_block_table", "ds_prefill_attn", "ds_decode_workspace_bytes", "ds_decode_attn", "ds_decode_attn_ex",
     "ds_kv_staging_bytes", "ds_kv_pack", "ds_kv_unpack", "ds_comm_get_unique_id", "ds_comm_init",
     "ds_comm_destroy", "ds_kv_migrate_staging_bytes", "ds_kv_migrate", "ds_ipc_export_mem", "ds_ipc_open_mem",
     "ds_ipc_close_mem", "ds_event_create_ipc", "ds_event_open_ipc", "ds_event_record", "ds_event_wait",
@@ -68,6 +69,8 @@ def _load():
                                     ctypes.c_int),
         "ds_decode_workspace_bytes": ([i32, i32, i32, i32], sz),
         "ds_decode_attn": ([P, P, P, P, cache_p, i32, P, i32, P, i32, i32, f32, P, sz, P], ctypes.c_int),
+        "ds_decode_attn_ex": ([P, P, P, P, cache_p, i32, P, i32, P, i32, i32, f32, P, sz, ctypes.c_uint32, P],
+                              ctypes.c_int),
         "ds_kv_staging_bytes": ([cache_p, i32, i32, i32], sz),
         "ds_kv_pack": ([cache_p, i32, i32, P, i32, i32, i32, P, sz, P], ctypes.c_int),
         "ds_kv_unpack": ([cache_p, i32, i32, P, i32, i32, i32, P, sz, P], ctypes.c_int),
@@ -291,7 +294,10 @@ def ds_decode_workspace_bytes(num_seqs: int, n_loc: int, head_dim: int, max_cach
 
 
 def ds_decode_attn(q, k_new, v_new, out, cache: KVCache, layer: int, block_table, cache_lens,
-                   max_cache_len: int, softmax_scale: float, workspace, stream=None):
+                   max_cache_len: int, softmax_scale: float, workspace, stream=None, early_kv: bool = False):
+    """early_kv=True: DS_DECODE_EARLY_KV (include/ds.h) — the caller guarantees the
+    kernel just ahead on the stream writes neither the lengths, the table nor this
+    layer's pages"""
     torch = _torch()
     for t, nm in ((q, "q"), (k_new, "k_new"), (v_new, "v_new"), (out, "out")):
         _dev(t, torch.bfloat16, nm)
@@ -302,10 +308,10 @@ def ds_decode_attn(q, k_new, v_new, out, cache: KVCache, layer: int, block_table
         raise ValueError("q must be [B][n_loc][head_dim] matching the cache")
     ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(),
                                                             workspace.numel() * workspace.element_size())
-    _check(_lib.ds_decode_attn(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), out.data_ptr(),
-                               cache.ref(), layer, block_table.data_ptr(), block_table.shape[1],
-                               cache_lens.data_ptr(), B, max_cache_len, softmax_scale, ws_ptr,
-                               ws_bytes, _stream(stream)))
+    _check(_lib.ds_decode_attn_ex(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), out.data_ptr(),
+                                  cache.ref(), layer, block_table.data_ptr(), block_table.shape[1],
+                                  cache_lens.data_ptr(), B, max_cache_len, softmax_scale, ws_ptr,
+                                  ws_bytes, DS_DECODE_EARLY_KV if early_kv else 0, _stream(stream)))
 
 
 # --------------------------------------------------------------------- a4 / a6

@@ -315,13 +315,14 @@ extern "C" size_t ds_decode_workspace_bytes(int32_t num_seqs, int32_t n_loc, int
   return decode_layout(num_seqs, n_loc, head_dim, kDecodeMaxSMs, max_cache_len).total;
 }
 
-extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void *v_new, void *out,
-                                    const ds_kv_cache *cache, int32_t layer,
-                                    const int32_t *block_table, int32_t max_blocks_per_seq,
-                                    const int32_t *cache_lens, int32_t num_seqs,
-                                    int32_t max_cache_len, float softmax_scale, void *workspace,
-                                    size_t workspace_bytes, void *stream) {
+extern "C" ds_status ds_decode_attn_ex(const void *q, const void *k_new, const void *v_new, void *out,
+                                       const ds_kv_cache *cache, int32_t layer,
+                                       const int32_t *block_table, int32_t max_blocks_per_seq,
+                                       const int32_t *cache_lens, int32_t num_seqs,
+                                       int32_t max_cache_len, float softmax_scale, void *workspace,
+                                       size_t workspace_bytes, uint32_t flags, void *stream) {
   const char *W = "ds_decode_attn";
+  if (flags & ~(uint32_t)DS_DECODE_EARLY_KV) return fail(DS_ERR_INVALID_ARG, "%s: unknown flags", W);
   if (num_seqs < 0) return fail(DS_ERR_INVALID_ARG, "%s: num_seqs < 0", W);
   if (ds_status s = check_cache(cache, W)) return s;
   if (num_seqs == 0) return DS_OK;
@@ -357,6 +358,7 @@ extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void
   a.chunk_rows = reinterpret_cast<float *>(wsb + L.chunk_off);
   a.max_chunks = L.max_chunks;
   a.max_cache_len = max_cache_len;
+  a.early_kv = (flags & DS_DECODE_EARLY_KV) ? 1 : 0;
   a.layer = layer;
   a.num_blocks = cache->num_blocks;
   a.n_loc = n;
@@ -366,6 +368,16 @@ extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void
   cudaError_t e = launch_decode(a, D, device_sms(), static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, W);
   return DS_OK;
+}
+
+extern "C" ds_status ds_decode_attn(const void *q, const void *k_new, const void *v_new, void *out,
+                                    const ds_kv_cache *cache, int32_t layer,
+                                    const int32_t *block_table, int32_t max_blocks_per_seq,
+                                    const int32_t *cache_lens, int32_t num_seqs,
+                                    int32_t max_cache_len, float softmax_scale, void *workspace,
+                                    size_t workspace_bytes, void *stream) {
+  return ds_decode_attn_ex(q, k_new, v_new, out, cache, layer, block_table, max_blocks_per_seq, cache_lens,
+                           num_seqs, max_cache_len, softmax_scale, workspace, workspace_bytes, 0u, stream);
 }
 
 // ----------------------------------------------------------- a4 / a6

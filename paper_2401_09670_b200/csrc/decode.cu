@@ -26,6 +26,9 @@
 //    them (a8, fused; atomic ticket per pair, self-resetting);
 //  * launched with programmatic dependent launch (griddepcontrol.wait before
 //    the first read), so launch latency overlaps the previous kernel's tail;
+//    with DS_DECODE_EARLY_KV the lengths, table and first pages are read before
+//    that wait (the caller vouches the previous kernel does not write them), so
+//    the opening page burst overlaps the previous kernel's drain;
 //  * the append (i) is fused: the warp that owns the page holding position c
 //    stores k_new/v_new into it and uses them from global memory for token c.
 #include "common.cuh"
@@ -403,7 +406,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
   // PDL: the launch and CTA set-up overlap the previous kernel's tail; nothing
   // written by an earlier kernel (lengths, tables, pages, workspace) is read
   // before this wait.
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const bool early = a.early_kv != 0;
+  if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) *reinterpret_cast<int *>(smem + C::kDoneOff) = 0;  // ordered by build_prefix's barriers
   DTRACE(0, gtimer());
   build_prefix(a.cache_lens, B, prefix);
@@ -505,6 +509,15 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs
     push_range(gw);
     for (int i = 0; i < C::kSlots && issue(); ++i) {
     }
+  }
+  if (early) {
+    // early_kv: the lengths, the table and this layer's pages were read above
+    // (and the first pages are in flight) before the previous kernel finished;
+    // q, k_new, v_new, the workspace and `out` only from here on. The next kernel
+    // may start once every CTA got here, so the kernel before this one is complete
+    // by the time the next one reads anything.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   }
 
   // consumer (its first range is the static one: computed here, not read from the

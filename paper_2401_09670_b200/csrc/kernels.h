@@ -23,6 +23,7 @@ struct DecodeArgs {
   int32_t *dyn;                       // [2]: chunk counter, finished warps (zero between launches)
   int64_t max_chunks;                 // capacity of chunk_rows
   int32_t max_cache_len;              // bound of cache_lens (host-side kernel choice)
+  int32_t early_kv;                   // read lengths / table / pages before the PDL wait
   int32_t layer, num_blocks, n_loc, max_blocks, num_seqs;
   float scale_log2;  // softmax_scale * log2(e)
 };

@@ -176,6 +176,10 @@ def test_decode_validation_and_workspace():
     assert call(543, None, 0) == ds.DS_ERR_INVALID_ARG  # needs split workspace
     assert call(640, FAKE, ws) == ds.DS_ERR_INVALID_ARG  # 640/16 >= 40 pages
     assert call(543, FAKE, ws) == ds.DS_ERR_CUDA
+    call_ex = lambda flags: lib.ds_decode_attn_ex(FAKE, FAKE, FAKE, FAKE, ctypes.byref(c), 0, FAKE, 40, FAKE, 1,
+                                                  543, 0.088, FAKE, ws, flags, None)
+    assert call_ex(2) == ds.DS_ERR_INVALID_ARG and "flags" in ds.ds_last_error()
+    assert call_ex(ds.DS_DECODE_EARLY_KV) == ds.DS_ERR_CUDA  # a valid call, no device here
 
 
 def test_decode_workspace_holds_the_dynamic_chunks():

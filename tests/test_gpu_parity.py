@@ -319,6 +319,76 @@ def test_decode_batch256_config3_shape_sampled(oracle_mod):
     assert max(errs) <= WARN, errs
 
 
+def _decode_layer_chain(oracle_mod, ctx, n, d, layers, seed, early, graph):
+    """Prefill `layers` layers of one pool, then one decode step over every layer,
+    back to back on one stream (optionally as one CUDA graph, whose PDL edges let
+    consecutive decode kernels overlap); returns per-layer outputs, the pool after
+    the appends, and the oracle's outputs."""
+    B = len(ctx)
+    maxb = _ceil(max(ctx) + 2, BS)
+    nblocks = sum(_ceil(c + 2, BS) for c in ctx) + 4
+    side = Side(oracle_mod, layers, nblocks, n, d)
+    t_ds = np.full((B, maxb), -1, np.int32)
+    t_or = t_ds.copy()
+    side.append([0] * B, ctx, t_ds, t_or)
+    scale = 1.0 / math.sqrt(d)
+    for layer in range(layers):
+        b = syn.prefill_batch(seed + layer, ctx, n, d)
+        out = torch.empty_like(to_dev(b.q))
+        ds.ds_prefill_attn(to_dev(b.q), to_dev(b.k), to_dev(b.v), out, i32(b.cu_seqlens), max(ctx), side.cache,
+                           layer, i32(t_ds), scale)
+        side.opool.write_prefill(layer, b.k, b.v, b.cu_seqlens, t_or)
+    side.append(ctx, [1] * B, t_ds, t_or)
+    dbs = [syn.decode_batch(seed * 10 + layer, B, n, d) for layer in range(layers)]
+    qs = [(to_dev(x.q), to_dev(x.k_new), to_dev(x.v_new)) for x in dbs]
+    outs = torch.full((layers, B, n, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    ws = torch.zeros(ds.ds_decode_workspace_bytes(B, n, d, max(ctx)), dtype=torch.uint8, device="cuda")
+    tab, lens = i32(t_ds), i32(ctx)
+    torch.cuda.synchronize()
+
+    def chain():
+        for layer in range(layers):
+            q, kn, vn = qs[layer]
+            ds.ds_decode_attn(q, kn, vn, outs[layer], side.cache, layer, tab, lens, max(ctx), scale, ws,
+                              early_kv=early)
+
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+            chain()
+        g.replay()
+    else:
+        chain()
+    torch.cuda.synchronize()
+    refs = [side.opool.decode(layer, dbs[layer].q, dbs[layer].k_new, dbs[layer].v_new, t_or, list(ctx), scale)
+            for layer in range(layers)]
+    return outs, side, t_ds, refs
+
+
+@pytest.mark.parametrize("ctx,n,d,graph", [
+    ([100, 543, 17, 1, 31], 4, 128, True),                           # static split, bitwise vs the plain call
+    ([int(x) for x in syn.rng(31).integers(300, 900, 384)], 16, 128, True),  # dynamic tail on
+    ([33, 1, 700], 2, 64, False),                                     # eager launches, d = 64
+])
+def test_decode_early_kv_layer_chain(oracle_mod, ctx, n, d, graph):
+    """DS_DECODE_EARLY_KV over a layer loop (the case the flag is for: each call
+    appends only to its own layer): per layer the outputs match the oracle, the
+    appends land, and — where no dynamic chunks make the merge order vary — the
+    bytes equal those of the plain call."""
+    layers = 4
+    outs, side, table, refs = _decode_layer_chain(oracle_mod, ctx, n, d, layers, 41, True, graph)
+    cur = [c + 1 for c in ctx]
+    for layer in range(layers):
+        err = oracle_mod.max_rel_err(to_f64(outs[layer]), refs[layer])
+        assert err <= WARN, (layer, err)
+        assert pages_match(to_bits(side.cache.tensor), side.opool, layer, cur, table)
+    if len(ctx) < 100:
+        outs0, side0, _, _ = _decode_layer_chain(oracle_mod, ctx, n, d, layers, 41, False, graph)
+        assert torch.equal(outs.view(torch.int16), outs0.view(torch.int16))
+        assert torch.equal(side.cache.tensor.view(torch.int16), side0.cache.tensor.view(torch.int16))
+
+
 # ------------------------------------------------------------------ a4 - a6
 def test_pack_unpack_loopback_bit_exact(oracle_mod):
     lens = [40, 17, 100]

@@ -95,6 +95,9 @@ def chunked_point(prefix, chunk, B, n, d, reps=20, rot=4):
             "frac_attainable": roof / t}
 
 
+EARLY = os.environ.get("DS_EARLY_KV", "1") != "0"  # DS_DECODE_EARLY_KV on layers > 0, as bench.py
+
+
 def decode_point(B, ctx, n, d, layers=8, reps=5):
     pages_per = -(-(ctx + 2) // 16)
     nb = B * pages_per + 8
@@ -112,7 +115,7 @@ def decode_point(B, ctx, n, d, layers=8, reps=5):
 
     def run():
         for l in range(layers):
-            ds.ds_decode_attn(q[l], q[l], q[l], out, cache, l, tab_d, cl, ctx, scale, ws)
+            ds.ds_decode_attn(q[l], q[l], q[l], out, cache, l, tab_d, cl, ctx, scale, ws, early_kv=l > 0 and EARLY)
 
     run()
     g = torch.cuda.CUDAGraph()
