@@ -6,7 +6,7 @@ import os
 import subprocess
 import sys
 
-POINTS = [(32, 544), (64, 544), (128, 544), (256, 544), (64, 2048), (16, 2048)]
+POINTS = [(int(b), int(c)) for b, c in (x.split('x') for x in os.environ.get('DS_POINTS', '32x544,64x544,128x544,256x544,64x2048,16x2048').split(','))]
 CHILD = r"""
 import json, sys
 sys.argv = ['kb']
