@@ -104,7 +104,9 @@ enum { DS_BT_APPEND = 0, DS_BT_FREE = 1 };
  * table_h: host int32 [num_seqs][max_blocks_per_seq], row-major, -1 = no page.
  * block_size must be 16. num_seqs == 0 is a no-op. num_free_h may be NULL.
  * Errors: DS_ERR_INVALID_ARG (negative lengths, ceil(len/bs) > max_blocks_per_seq,
- * FREE of an id that is not allocated), DS_ERR_NO_BLOCKS. */
+ * FREE of an id that is not allocated or that appears twice in the call; a
+ * rejected FREE frees nothing), DS_ERR_NO_BLOCKS, DS_ERR_STATE (free set
+ * inconsistent; nothing allocated). */
 ds_status ds_block_table(ds_pool pool, int32_t op, int32_t num_seqs,
                          const int32_t *cur_lens_h, const int32_t *add_lens_h,
                          int32_t *table_h, int32_t max_blocks_per_seq,
@@ -206,7 +208,11 @@ ds_status ds_prefill_attn_chunked(const void *q, const void *k, const void *v, v
  *               aligned, caller-owned. It must be ZEROED once before its first
  *               use (e.g. torch.zeros); every call leaves it zeroed again (it
  *               holds split partials and self-resetting merge tickets). Calls
- *               sharing a workspace must be ordered on one stream.
+ *               sharing a workspace must be ordered on one stream. The merge
+ *               tickets and counters sit in a fixed region at a fixed offset, so
+ *               one workspace may serve calls of any batch, head count, head_dim
+ *               or length as long as it is large enough for each call.
+ * Limits      : num_seqs <= 4096 and num_seqs * n_loc <= 524288 (DS_ERR_INVALID_ARG).
  * Work split: the (seq, head, page) space is cut into equal page ranges, one
  * per warp of a persistent grid; a pair that straddles ranges is merged from
  * its partials (m, l, o) with the log-sum-exp rule (a8), inside the same launch.

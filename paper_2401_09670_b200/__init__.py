@@ -146,6 +146,29 @@ def _dev(t, dtype, name):
     return t
 
 
+def _check_activations(q, others, cache, what="T"):
+    """q [rows][n_loc][head_dim] matching the cache; every tensor in `others` the
+    same shape (the C side cannot see device array sizes: a mismatch here would be
+    an out-of-bounds device access there)"""
+    if q.dim() != 3 or q.shape[1] != cache.heads or q.shape[2] != cache.head_dim:
+        raise ValueError(f"q must be [{what}][n_loc][head_dim] matching the cache")
+    for t, nm in others:
+        if t.shape != q.shape:
+            raise ValueError(f"{nm} must have q's shape {tuple(q.shape)}, got {tuple(t.shape)}")
+
+
+def _check_table(table, rows: int, name: str):
+    if table.dim() != 2 or table.shape[0] < rows:
+        raise ValueError(f"{name} must be 2-D with at least {rows} rows, got {tuple(table.shape)}")
+
+
+def _check_seqlens(cu_seqlens, T: int, q_rows: int):
+    if cu_seqlens.dim() != 1 or cu_seqlens.numel() < 1:
+        raise ValueError("cu_seqlens must be 1-D [num_seqs + 1]")
+    if T > q_rows:
+        raise ValueError(f"total_tokens {T} exceeds the {q_rows} rows of q")
+
+
 class KVCache:
     """Caller-owned paged KV pool of one rank: bf16 [L][2][num_blocks][n][16][D]."""
 
@@ -233,11 +256,9 @@ def ds_prefill_attn(q, k, v, out, cu_seqlens, max_seqlen: int, cache: KVCache, l
     _dev(cu_seqlens, torch.int32, "cu_seqlens")
     _dev(block_table, torch.int32, "block_table")
     T = q.shape[0] if total_tokens is None else total_tokens
-    if q.dim() != 3 or q.shape[1] != cache.heads or q.shape[2] != cache.head_dim:
-        raise ValueError("q must be [T][n_loc][head_dim] matching the cache")
-    for t in (k, v, out):
-        if t.shape != q.shape:
-            raise ValueError("q, k, v, out must have the same shape")
+    _check_activations(q, ((k, "k"), (v, "v"), (out, "out")), cache)
+    _check_seqlens(cu_seqlens, T, q.shape[0])
+    _check_table(block_table, cu_seqlens.numel() - 1, "block_table")
     _check(_lib.ds_prefill_attn(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                 cu_seqlens.data_ptr(), cu_seqlens.numel() - 1, T, max_seqlen,
                                 cache.ref(), layer, block_table.data_ptr(), block_table.shape[1],
@@ -257,11 +278,10 @@ def ds_prefill_attn_push(q, k, v, out, cu_seqlens, max_seqlen: int, cache: KVCac
     _dev(block_table, torch.int32, "block_table")
     _dev(dst_block_table, torch.int32, "dst_block_table")
     T = q.shape[0] if total_tokens is None else total_tokens
-    if q.dim() != 3 or q.shape[1] != cache.heads or q.shape[2] != cache.head_dim:
-        raise ValueError("q must be [T][n_loc][head_dim] matching the cache")
-    for t in (k, v, out):
-        if t.shape != q.shape:
-            raise ValueError("q, k, v, out must have the same shape")
+    _check_activations(q, ((k, "k"), (v, "v"), (out, "out")), cache)
+    _check_seqlens(cu_seqlens, T, q.shape[0])
+    _check_table(block_table, cu_seqlens.numel() - 1, "block_table")
+    _check_table(dst_block_table, cu_seqlens.numel() - 1, "dst_block_table")
     _check(_lib.ds_prefill_attn_push(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                      cu_seqlens.data_ptr(), cu_seqlens.numel() - 1, T, max_seqlen, cache.ref(), layer,
                                      block_table.data_ptr(), block_table.shape[1], dst_cache.ref(), dst_layer,
@@ -279,8 +299,12 @@ def ds_prefill_attn_chunked(q, k, v, out, cu_seqlens, prefix_lens, max_chunk_len
     _dev(cu_seqlens, torch.int32, "cu_seqlens")
     _dev(prefix_lens, torch.int32, "prefix_lens")
     _dev(block_table, torch.int32, "block_table")
-    if q.dim() != 3 or q.shape[1] != cache.heads or q.shape[2] != cache.head_dim:
-        raise ValueError("q must be [T][n_loc][head_dim] matching the cache")
+    _check_activations(q, ((k, "k"), (v, "v"), (out, "out")), cache)
+    _check_seqlens(cu_seqlens, q.shape[0], q.shape[0])
+    B = cu_seqlens.numel() - 1
+    if prefix_lens.dim() != 1 or prefix_lens.numel() < B:
+        raise ValueError(f"prefix_lens must be 1-D with at least {B} entries")
+    _check_table(block_table, B, "block_table")
     _check(_lib.ds_prefill_attn_chunked(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
                                         cu_seqlens.data_ptr(), prefix_lens.data_ptr(), cu_seqlens.numel() - 1,
                                         q.shape[0], max_chunk_len, max_context_len, cache.ref(), layer,
@@ -304,8 +328,10 @@ def ds_decode_attn(q, k_new, v_new, out, cache: KVCache, layer: int, block_table
     _dev(block_table, torch.int32, "block_table")
     _dev(cache_lens, torch.int32, "cache_lens")
     B = q.shape[0]
-    if q.dim() != 3 or q.shape[1] != cache.heads or q.shape[2] != cache.head_dim:
-        raise ValueError("q must be [B][n_loc][head_dim] matching the cache")
+    _check_activations(q, ((k_new, "k_new"), (v_new, "v_new"), (out, "out")), cache, "B")
+    if cache_lens.dim() != 1 or cache_lens.numel() < B:
+        raise ValueError(f"cache_lens must be 1-D with at least {B} entries")
+    _check_table(block_table, B, "block_table")
     ws_ptr, ws_bytes = (None, 0) if workspace is None else (workspace.data_ptr(),
                                                             workspace.numel() * workspace.element_size())
     _check(_lib.ds_decode_attn_ex(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), out.data_ptr(),

@@ -328,6 +328,8 @@ extern "C" ds_status ds_decode_attn_ex(const void *q, const void *k_new, const v
   if (num_seqs == 0) return DS_OK;
   if (num_seqs > kDecodeMaxSeqs)
     return fail(DS_ERR_INVALID_ARG, "%s: at most %d sequences per call", W, kDecodeMaxSeqs);
+  if ((int64_t)num_seqs * cache->num_heads > kDecodeMaxPairs)
+    return fail(DS_ERR_INVALID_ARG, "%s: num_seqs * n_loc must be <= %d", W, kDecodeMaxPairs);
   if (!q || !k_new || !v_new || !out || !block_table || !cache_lens)
     return fail(DS_ERR_INVALID_ARG, "%s: NULL pointer argument", W);
   if (!aligned16(q) || !aligned16(k_new) || !aligned16(v_new) || !aligned16(out))
@@ -392,7 +394,7 @@ ds_status kv_copy_checked(const ds_kv_cache *cache, int32_t layer_begin, int32_t
                           const int32_t *block_ids, int32_t num_blocks, int32_t head_begin,
                           int32_t head_count, void *staging, size_t staging_bytes,
                           int64_t row_begin, int64_t row_end, bool pack, cudaStream_t stream,
-                          const char *W) {
+                          const char *W, bool dry_run = false) {
   if (ds_status s = check_cache(cache, W)) return s;
   if (layer_count < 0 || num_blocks < 0 || head_count < 0)
     return fail(DS_ERR_INVALID_ARG, "%s: negative count", W);
@@ -408,6 +410,7 @@ ds_status kv_copy_checked(const ds_kv_cache *cache, int32_t layer_begin, int32_t
   if (staging_bytes < (size_t)(row_end - row_begin) * row_bytes)
     return fail(DS_ERR_INVALID_ARG, "%s: staging_bytes too small", W);
   if (ds_status s = require_sm100(W)) return s;
+  if (dry_run) return DS_OK;  // every check passed; the caller launches later
   KvCopyArgs a{};
   a.cache = static_cast<uint16_t *>(cache->base);
   a.staging = static_cast<uint16_t *>(staging);

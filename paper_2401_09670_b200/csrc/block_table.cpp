@@ -41,6 +41,11 @@ struct ds_pool_s {
     return -1;
   }
   bool is_free(int32_t id) const { return (words[id >> 6] >> (id & 63)) & 1ull; }
+  void clear_free(int32_t id) {  // undo set_free (rollback of a rejected call)
+    const int32_t w = id >> 6;
+    words[w] &= ~(1ull << (id & 63));
+    if (!words[w]) summary[w >> 6] &= ~(1ull << (w & 63));
+  }
 };
 
 static int32_t blocks_for(int64_t tokens, int32_t bs) { return (int32_t)((tokens + bs - 1) / bs); }
@@ -96,33 +101,54 @@ extern "C" ds_status ds_block_table(ds_pool pool, int32_t op, int32_t num_seqs,
       need += nb_new - nb_old;
     }
     if (need > pool->num_free) return ds::fail(DS_ERR_NO_BLOCKS, "ds_block_table: pool exhausted (nothing allocated)");
+    std::vector<int64_t> slots;  // table entries written so far (rollback if the free set is inconsistent)
+    slots.reserve((size_t)need);
     for (int32_t s = 0; s < num_seqs; ++s) {
       const int32_t nb_old = blocks_for(cur_lens_h[s], block_size);
       const int32_t nb_new = blocks_for((int64_t)cur_lens_h[s] + add_lens_h[s], block_size);
       for (int32_t b = nb_old; b < nb_new; ++b) {
-        table_h[(int64_t)s * max_blocks_per_seq + b] = pool->take_lowest();
+        const int32_t id = pool->take_lowest();
+        if (id < 0) {  // cannot happen while num_free is exact; never write -1 into a table
+          for (int64_t e : slots) {
+            pool->set_free(table_h[e]);
+            table_h[e] = -1;
+          }
+          pool->num_free += (int32_t)slots.size();
+          return ds::fail(DS_ERR_STATE, "ds_block_table: free set inconsistent with num_free (nothing allocated)");
+        }
+        const int64_t e = (int64_t)s * max_blocks_per_seq + b;
+        table_h[e] = id;
+        slots.push_back(e);
         pool->num_free--;
       }
     }
   } else {
+    // validate by freeing tentatively: an id that is out of range, not allocated,
+    // or listed twice in this call (already freed a moment ago) rolls the call back
+    std::vector<int32_t> freed;
     for (int32_t s = 0; s < num_seqs; ++s) {
       const int32_t nb = blocks_for(cur_lens_h[s], block_size);
-      if (cur_lens_h[s] < 0 || nb > max_blocks_per_seq)
-        return ds::fail(DS_ERR_INVALID_ARG, "ds_block_table: bad length in FREE");
-      for (int32_t b = 0; b < nb; ++b) {
+      bool bad = cur_lens_h[s] < 0 || nb > max_blocks_per_seq;
+      for (int32_t b = 0; !bad && b < nb; ++b) {
         const int32_t id = table_h[(int64_t)s * max_blocks_per_seq + b];
-        if (id < 0 || id >= pool->num_blocks || pool->is_free(id))
-          return ds::fail(DS_ERR_INVALID_ARG, "ds_block_table: FREE of a page that is not allocated");
+        if (id < 0 || id >= pool->num_blocks || pool->is_free(id)) {
+          bad = true;
+          break;
+        }
+        pool->set_free(id);
+        freed.push_back(id);
+      }
+      if (bad) {
+        for (int32_t id : freed) pool->clear_free(id);
+        return ds::fail(DS_ERR_INVALID_ARG,
+                        "ds_block_table: bad length in FREE, or FREE of a page that is not allocated "
+                        "(or listed twice); nothing freed");
       }
     }
+    pool->num_free += (int32_t)freed.size();
     for (int32_t s = 0; s < num_seqs; ++s) {
       const int32_t nb = blocks_for(cur_lens_h[s], block_size);
-      for (int32_t b = 0; b < nb; ++b) {
-        int32_t &e = table_h[(int64_t)s * max_blocks_per_seq + b];
-        pool->set_free(e);
-        pool->num_free++;
-        e = -1;
-      }
+      for (int32_t b = 0; b < nb; ++b) table_h[(int64_t)s * max_blocks_per_seq + b] = -1;
     }
   }
   if (num_free_h) *num_free_h = pool->num_free;

@@ -663,16 +663,19 @@ extern "C" __attribute__((visibility("default"))) int ds_debug_decode_trace(unsi
 }
 #endif
 
-// workspace: [dyn counters 16 B][static partial rows][tickets B x n][chunk partial rows]
-// (counters and tickets at offsets that do not depend on the lengths: they must
-// stay zero between calls; the chunk rows need no initialisation)
+// workspace: [dyn counters 16 B][tickets kDecodeMaxPairs x int32][static partial rows]
+// [chunk partial rows]. The counters and tickets must be zero between calls: both sit
+// at offsets and in regions that depend on nothing about the call (batch, heads,
+// head_dim, lengths), so a workspace reused with a growing batch or another head_dim
+// still finds every ticket it touches at zero. The partial rows need no
+// initialisation (written before they are read in every launch).
 DecodeLayout decode_layout(int num_seqs, int n_loc, int head_dim, int num_sms, int max_cache_len) {
   DecodeLayout L;
   const size_t row = (size_t)(head_dim + 4) * sizeof(float);
   L.dyn_off = 0;
-  L.rows_off = 16;
-  L.tickets_off = L.rows_off + (size_t)num_sms * kWarps * 2 * row;
-  L.chunk_off = (L.tickets_off + (size_t)num_seqs * n_loc * 4 + 15) & ~(size_t)15;
+  L.tickets_off = 16;
+  L.rows_off = L.tickets_off + (size_t)kDecodeMaxPairs * 4;
+  L.chunk_off = L.rows_off + (size_t)num_sms * kWarps * 2 * row;
   const int64_t pmax = (int64_t)num_seqs * n_loc * npages_of(max_cache_len);
   const Part q = make_part(pmax, (int64_t)num_sms * kWarps, INT64_MAX / kChunkPages);
   L.max_chunks = q.NC;

@@ -11,6 +11,10 @@ namespace ds {
 // a7 + a8
 constexpr int kDecodeMaxSeqs = 4096;  // sequences per decode launch (smem page prefix)
 constexpr int kDecodeMaxSMs = 160;    // workspace is sized for grids up to this many CTAs
+// merge tickets: a fixed region of this many (seq, head) pairs at a fixed offset of
+// every decode workspace, so a call with another batch shape or head_dim finds the
+// tickets of every pair it can touch at zero (they are reset by their merger)
+constexpr int kDecodeMaxPairs = 1 << 19;  // 2 MiB: 4096 sequences x 128 heads
 struct DecodeArgs {
   const uint16_t *q, *k_new, *v_new;  // bf16 [B][n][D]
   void *out;                          // bf16 [B][n][D]
@@ -18,7 +22,7 @@ struct DecodeArgs {
   const int32_t *block_table;         // [B][max_blocks]
   const int32_t *cache_lens;          // [B]
   float *workspace;                   // [warps][2][D+4] straddling-pair partials (o, m, l, pad)
-  int32_t *tickets;                   // [B][n] merge tickets (zero between launches)
+  int32_t *tickets;                   // [kDecodeMaxPairs] merge tickets, pair b*n+h (zero between launches)
   float *chunk_rows;                  // [chunks][2][D+4] partials of the dynamically taken chunks
   int32_t *dyn;                       // [2]: chunk counter, finished warps (zero between launches)
   int64_t max_chunks;                 // capacity of chunk_rows

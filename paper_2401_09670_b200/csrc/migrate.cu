@@ -28,7 +28,7 @@ ds_status kv_copy_checked(const ds_kv_cache *cache, int32_t layer_begin, int32_t
                           const int32_t *block_ids, int32_t num_blocks, int32_t head_begin,
                           int32_t head_count, void *staging, size_t staging_bytes,
                           int64_t row_begin, int64_t row_end, bool pack, cudaStream_t stream,
-                          const char *W);
+                          const char *W, bool dry_run = false);
 }  // namespace ds
 
 using namespace ds;
@@ -241,6 +241,17 @@ extern "C" ds_status ds_kv_migrate(ds_comm comm, int32_t role, int32_t peer,
   const int32_t dst_h0 = role == DS_MIGRATE_SELF ? dst_head_begin : head_begin;
   char *recv_base = role == DS_MIGRATE_SELF ? stg + 2 * slot_bytes : stg;
 
+  // every pack / unpack launch of the loop below is checked once up front (device,
+  // pool, ranges, staging), so a rejected call posts no send or receive and leaves
+  // both streams and the peer untouched
+  if (send_side)
+    if (ds_status s = kv_copy_checked(src, layer_begin, layer_count, block_ids, num_blocks, head_begin,
+                                      head_count, stg, slot_bytes, 0, crows, true, A, W, true))
+      return s;
+  if (role != DS_MIGRATE_SEND)
+    if (ds_status s = kv_copy_checked(dst, layer_begin, layer_count, dst_ids, num_blocks, dst_h0, head_count,
+                                      recv_base, slot_bytes, 0, crows, false, A, W, true))
+      return s;
   DS_CUDA(cudaEventRecord(comm->ev_start, A), W);
   DS_CUDA(cudaStreamWaitEvent(B, comm->ev_start, 0), W);
   for (int64_t k = 0; k < nchunks; ++k) {

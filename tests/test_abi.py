@@ -122,6 +122,30 @@ def test_block_table_rejects_bad_args():
     assert pool.num_free == 8
 
 
+def test_block_table_free_rejects_duplicate_ids():
+    """the same page listed twice in one FREE must not be freed twice
+    (num_free would overcount and a later APPEND would hand out page -1)."""
+    pool = ds.Pool(8)
+    t = np.full((2, 2), -1, np.int32)
+    ds.ds_block_table(pool, ds.DS_BT_APPEND, [0, 0], [32, 16], t)  # pages 0,1 | 2
+    assert pool.num_free == 5
+    dup = np.array([[0, 1], [1, -1]], np.int32)  # page 1 in both rows
+    with pytest.raises(ds.DSError) as ei:
+        ds.ds_block_table(pool, ds.DS_BT_FREE, [32, 16], None, dup)
+    assert ei.value.status == ds.DS_ERR_INVALID_ARG
+    assert pool.num_free == 5 and np.array_equal(dup, [[0, 1], [1, -1]])  # nothing freed
+    same_row = np.array([[2, 2]], np.int32)
+    with pytest.raises(ds.DSError):
+        ds.ds_block_table(pool, ds.DS_BT_FREE, [32], None, same_row)
+    assert pool.num_free == 5
+    # the pool is intact: the real tables free cleanly and everything is allocatable again
+    ds.ds_block_table(pool, ds.DS_BT_FREE, [32, 16], None, t)
+    assert pool.num_free == 8 and np.all(t == -1)
+    full = np.full((1, 8), -1, np.int32)
+    ds.ds_block_table(pool, ds.DS_BT_APPEND, [0], [128], full)
+    assert sorted(full[0].tolist()) == list(range(8)) and pool.num_free == 0
+
+
 def _cache(base=0x10000, L=2, NB=64, n=4, D=64):
     return ds.ds_kv_cache(base, L, NB, n, 16, D)
 
@@ -196,6 +220,48 @@ def test_decode_workspace_holds_the_dynamic_chunks():
     base = f(big_b, 40, 128, 0)  # one page per sequence: static
     assert f(big_b, 40, 128, 543) == base + chunks * 2 * (128 + 4) * 4
     assert f(big_b, 40, 128, 1000) > f(big_b, 40, 128, 543)  # more pages -> more chunk rows
+
+
+def test_decode_workspace_tickets_fixed_region():
+    """the merge tickets live in one fixed region at a fixed
+    offset, so a workspace reused by calls with other batch shapes or head_dim never
+    finds its tickets on top of another call's partial rows. The size therefore has
+    a fixed 2 MiB ticket part (4096 x 128 pairs) plus parts that grow with the call."""
+    f = ds.ds_decode_workspace_bytes
+    fixed = 16 + (1 << 19) * 4
+    rows = 160 * 16 * 2 * (128 + 4) * 4  # static partial rows of the largest grid
+    assert f(1, 1, 128, 0) == fixed + rows
+    assert f(1000, 100, 128, 0) == fixed + rows  # the ticket part does not grow (no dynamic chunks here)
+    lib = ds.lib()
+    c = _cache(n=256, D=128, NB=4096)
+    ws = f(4096, 256, 128, 15)
+    call = lambda B: lib.ds_decode_attn(FAKE, FAKE, FAKE, FAKE, ctypes.byref(c), 0, FAKE, 40, FAKE, B, 15, 0.088,
+                                        FAKE, ws, None)
+    assert call(2048) == ds.DS_ERR_CUDA          # 2048 x 256 = 2^19 pairs: accepted (no device here)
+    assert call(2049) == ds.DS_ERR_INVALID_ARG   # one pair over the ticket region
+    assert "n_loc" in ds.ds_last_error()
+
+
+def test_wrapper_shape_checks():
+    """the Python wrappers reject shape mismatches the C side cannot
+    see (device array sizes) before any pointer crosses the boundary"""
+    import torch
+
+    class FakeCache:
+        heads, head_dim = 4, 64
+    q = torch.zeros(8, 4, 64)
+    ds._check_activations(q, ((torch.zeros(8, 4, 64), "k"),), FakeCache)
+    with pytest.raises(ValueError, match="k_new"):
+        ds._check_activations(q, ((torch.zeros(7, 4, 64), "k_new"),), FakeCache)
+    with pytest.raises(ValueError, match="matching the cache"):
+        ds._check_activations(torch.zeros(8, 5, 64), (), FakeCache)
+    with pytest.raises(ValueError, match="block_table"):
+        ds._check_table(torch.zeros(3, 4), 4, "block_table")
+    with pytest.raises(ValueError, match="block_table"):
+        ds._check_table(torch.zeros(12), 4, "block_table")
+    ds._check_table(torch.zeros(5, 4), 4, "block_table")
+    with pytest.raises(ValueError, match="total_tokens"):
+        ds._check_seqlens(torch.zeros(3), 9, 8)
 
 
 def test_staging_sizes():

@@ -199,7 +199,7 @@ def test_bench_step_shape_fused_prefill_then_dynamic_decode(oracle_mod):
 
 # ------------------------------------------------------------------ a7 + a8
 def run_decode(oracle_mod, ctx, n, d, seed=0, steps=1, fragment=0, q_sigma=1.0, max_cache_len=None,
-               table_cols=0, poison=False):
+               table_cols=0, poison=False, ws=None):
     """Prefill (GPU) the first ctx tokens of each sequence, then `steps` decode
     steps; compare each step with the oracle's decode."""
     B = len(ctx)
@@ -230,8 +230,9 @@ def run_decode(oracle_mod, ctx, n, d, seed=0, steps=1, fragment=0, q_sigma=1.0, 
     errs = []
     scale = 1.0 / math.sqrt(d)
     # one zeroed workspace reused by every step: the merge tickets must self-reset
-    ws = torch.zeros(max(ds.ds_decode_workspace_bytes(B, n, d, max(total)), 16) // 4 + 4,
-                     dtype=torch.float32, device="cuda")
+    if ws is None:
+        ws = torch.zeros(max(ds.ds_decode_workspace_bytes(B, n, d, max(total)), 16) // 4 + 4,
+                         dtype=torch.float32, device="cuda")
     for s in range(steps):
         side.append(cur, [1] * B, t_ds, t_or)
         db = syn.decode_batch(seed * 100 + s, B, n, d, q_sigma=q_sigma)
@@ -297,6 +298,27 @@ def test_decode_dynamic_chunks_ragged_d64(oracle_mod):
     side, table, cur, errs = run_decode(oracle_mod, ctx, 24, 64, seed=22, steps=2, fragment=7)
     assert max(errs) <= WARN, errs
     assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
+
+
+def test_decode_workspace_reused_across_batch_shapes(oracle_mod):
+    """ONE workspace, zeroed once, serves calls whose batch, head
+    count and head_dim change — growing batches that take the dynamic tail (whose
+    chunk partial rows are left non-zero) followed by bigger ones and another
+    head_dim. Every call must match the oracle: the merge tickets sit in a fixed
+    region, so no call finds them on top of an earlier call's partial rows."""
+    g = syn.rng(31)
+    calls = [
+        ([int(x) for x in g.integers(300, 900, 512)], 16, 128),   # dynamic tail
+        ([int(x) for x in g.integers(300, 900, 700)], 24, 128),   # more pairs, dynamic tail
+        ([int(x) for x in g.integers(0, 700, 96)], 8, 64),        # another head_dim
+        ([int(x) for x in g.integers(300, 1200, 600)], 24, 64),   # dynamic tail at head_dim 64
+        ([int(x) for x in g.integers(300, 900, 512)], 16, 128),   # the first shape again
+    ]
+    need = max(ds.ds_decode_workspace_bytes(len(c), n, d, max(c) + 2) for c, n, d in calls)
+    ws = torch.zeros(need // 4 + 4, dtype=torch.float32, device="cuda")
+    for i, (ctx, n, d) in enumerate(calls):
+        _, _, _, errs = run_decode(oracle_mod, ctx, n, d, seed=40 + i, steps=2, ws=ws)
+        assert max(errs) <= WARN, (i, errs)
 
 
 def test_decode_partition_invariance(oracle_mod):
