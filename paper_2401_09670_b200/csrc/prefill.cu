@@ -51,12 +51,6 @@ constexpr float kRescaleLog2 = 8.f;             // move the exponent base only p
 #define DS_PF_SLEEP_NS 0
 #endif
 constexpr int kPolyEvery = DS_PF_POLY_EVERY;    // 1 in kPolyEvery exp2 on the FMA pipe (ex2_poly)
-#ifndef DS_PF_QTMEM
-#define DS_PF_QTMEM 0
-#endif
-// Q as the TMEM operand of S = Q K^T (A/B variant): TMEM = Q [0,64) | S [64,128) |
-// O [128,256); one S buffer; the S MMA reads only K from smem
-constexpr bool kQT = DS_PF_QTMEM != 0;
 
 template <int D>
 struct Smem {
@@ -69,7 +63,7 @@ struct Smem {
   static constexpr uint32_t PREF = OST + 4 * 2048;     // int[kCompactSeqs + 1] tile prefix + 8 warp totals
   static constexpr uint32_t CLC = PREF + (kCompactSeqs + 1 + 8) * 4 + 12;  // 2 x 16-B work-stealing responses
   static constexpr uint32_t BAR = CLC + 32;
-  static constexpr uint32_t kBars = 22;
+  static constexpr uint32_t kBars = 21;
   static constexpr uint32_t TMEM_SLOT = BAR + kBars * 8;
   static constexpr uint32_t TOTAL = TMEM_SLOT + 16;
   static constexpr uint32_t ALLOC = TOTAL + 1024;  // slack for 1024-B alignment
@@ -89,7 +83,6 @@ enum {
   B_OE = 16,    // O read out by the epilogue (128 softmax threads, once per item)
   B_CLC = 17,   // [2] work-stealing response landed
   B_CLCE = 19,  // [2] response read by all 6 warps
-  B_QT = 21,    // kQT: Q copied smem -> TMEM by the 128 softmax threads (once per item)
 };
 
 // Persistent via cluster launch control: the grid keeps one CTA per (q tile, head,
@@ -221,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (threadIdx.x == 0) {
     for (int b = 0; b < (int)S::kBars; ++b) {
-      const bool per_thread = b == B_P || b == B_P + 1 || b == B_OE || b == B_QT;
+      const bool per_thread = b == B_P || b == B_P + 1 || b == B_OE;
       mbar_init(&bars[b], per_thread ? 128 : (b == B_CLCE || b == B_CLCE + 1) ? kThreads / 32 : 1);
     }
     fence_barrier_init();
@@ -237,9 +230,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tO = tmem + 128;
-  const uint32_t tQ = tmem, tS1 = tmem + 64;  // kQT layout (single S buffer at tS1)
-  // S buffer of tile g: kQT has one (at column 64), else S0 | S1 at columns 0 | 64
-  auto s_col = [&](uint32_t g) -> uint32_t { return kQT ? tS1 : tmem + (g & 1) * kBN; };
   if (warp == 4 && lane == 0) {
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_kv);
@@ -294,9 +284,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ------------------------------------------------------------ producer
         __syncwarp();  // elect.sync needs the whole warp converged (lane 0 issued the CLC request)
         if (elect_one()) {
-          // the previous item's Q is no longer read from smem: its S MMAs are done with it
-          // (kQT: the softmax threads copied it into TMEM)
-          if (it > 0) ctl_wait(&bars[kQT ? B_QT : B_QE], (it - 1) & 1);
+          if (it > 0) ctl_wait(&bars[B_QE], (it - 1) & 1);  // the previous item's S MMAs are done with Q
           mbar_arrive_expect_tx(&bars[B_Q], S::kQTile);
 #pragma unroll
           for (int c = 0; c < kChunks; ++c)
@@ -389,43 +377,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // this thread never waits on them (in-order tcgen05.mma execution orders every
         // S_g after the P_{g-2} V_{g-2} that reads its buffer).
         __syncwarp();
-        if (kQT && elect_one()) {
-          // One S buffer: S_g = Q K_g^T (Q from TMEM, K from smem), then — once the
-          // softmax has turned S_g into P_g — O += P_g V_g, then S_{g+1} (in-order
-          // execution: S_{g+1} overwrites P_g only after P_g V_g has read it). The
-          // commit of S_g also covers P_{g-1} V_{g-1}, so the softmax sees a stable O.
-          // B_QT (Q in TMEM) also tells that the previous item's O was read out.
-          constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
-          constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, D, 0, 1);
-          ctl_wait(&bars[B_QT], it & 1);
-          for (int j = 0; j < ntiles; ++j) {
-            const uint32_t g = g0 + j;
-            const int st = g & 1;
-            ctl_wait(&bars[B_KF + st], (g >> 1) & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk)
-              umma_ts(tS1, tQ + kk * 8,
-                      smem_desc_sw128(sbase + S::K0 + st * S::kKVTile + (kk >> 2) * kChunkBytes64 + (kk & 3) * 32,
-                                      16, 1024),
-                      idesc_s, kk > 0);
-            umma_commit(&bars[B_SF]);
-            umma_commit(&bars[B_KE + st]);
-            TRACE(T_MMA_S, g);
-            TRACE(T_MMA_WAIT_P, g);
-            ctl_wait(&bars[B_P], g & 1);
-            ctl_wait(&bars[B_VF + st], (g >> 1) & 1);
-            tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < kBN / 16; ++kk)
-              umma_ts(tO, tS1 + kk * 8,
-                      smem_desc_sw128(sbase + S::V0 + st * S::kKVTile + kk * 16 * 128, kChunkBytes64, 1024), idesc_o,
-                      (j > 0 || kk > 0));
-            umma_commit(&bars[B_VE + st]);
-            TRACE(T_MMA_PV, g);
-          }
-          umma_commit(&bars[B_O]);
-        } else if (!kQT && elect_one()) {
+        if (elect_one()) {
           constexpr uint32_t idesc_s = idesc_bf16_f32(kBM, kBN, 0, 0);
           constexpr uint32_t idesc_o = idesc_bf16_f32(kBM, D, 0, 1);
           ctl_wait(&bars[B_Q], it & 1);
@@ -483,42 +435,16 @@ __global__ void __launch_bounds__(kThreads, 2)
         // phase of both barriers in order, one tile of slack), and on P_{g-1} V_{g-1}
         // only to rescale O, and on the last P.V in the epilogue.
         auto wait_pv = [&](uint32_t k) { mbar_wait(&bars[B_O + (k & 1)], (k >> 1) & 1); };
-        if (kQT) {
-          // Q row -> TMEM lane `row` (the A operand of S = Q K^T): 16-B chunks of the
-          // SW128 smem tile (chunk k of row r at (k ^ (r & 7)) * 16), packed bf16 pairs
-          // in columns [0, D/2); then the producer may reload the smem tile.
-          mbar_wait(&bars[B_Q], it & 1);
-#pragma unroll
-          for (int c = 0; c < kChunks; ++c) {
-            uint32_t qv[32];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const uint4 v = *reinterpret_cast<const uint4 *>(smem + S::Q + c * kChunkBytes128 + row * 128 +
-                                                               ((k ^ (row & 7)) << 4));
-              qv[4 * k] = v.x;
-              qv[4 * k + 1] = v.y;
-              qv[4 * k + 2] = v.z;
-              qv[4 * k + 3] = v.w;
-            }
-            tmem_st32(tQ + lane_off + c * 32, qv);
-          }
-          tmem_wait_st();
-          tc_fence_before();
-          mbar_arrive(&bars[B_QT]);
-        }
         for (int j = 0; j < ntiles; ++j) {
           const uint32_t g = g0 + j;
           const int st = g & 1;
           if (threadIdx.x == 0) TRACE(T_SM_WAIT_S, g);
-          if (kQT)
-            mbar_wait(&bars[B_SF], g & 1);
-          else
-            mbar_wait(&bars[B_SF + st], (g >> 1) & 1);
+          mbar_wait(&bars[B_SF + st], (g >> 1) & 1);
           if (threadIdx.x == 0) TRACE(T_SM_GOT_S, g);
           tc_fence_after();
           uint32_t sr[2][32];
-          tmem_ld32(s_col(g) + lane_off, sr[0]);
-          tmem_ld32(s_col(g) + lane_off + 32, sr[1]);
+          tmem_ld32(tmem + lane_off + st * kBN, sr[0]);
+          tmem_ld32(tmem + lane_off + st * kBN + 32, sr[1]);
           tmem_wait_ld();
           // row max on the raw scores (scale > 0 preserves order); prefix tiles: keys at
           // or beyond c0 are not cached yet (masked); chunk tiles: causal within the
@@ -585,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           l = l * alpha + (rs0 + rs1);
           m = m_new;
           if (j > 0 && __any_sync(0xffffffffu, grow)) {  // warp-uniform O rescale, only when a base moved
-            if (!kQT) wait_pv(g - 1);                    // O is not in use by P_{g-1} V_{g-1} any more
+            wait_pv(g - 1);                              // O is not in use by P_{g-1} V_{g-1} any more
             tc_fence_after();
 #pragma unroll
             for (int cc = 0; cc < D / 32; ++cc) {
@@ -603,12 +529,12 @@ __global__ void __launch_bounds__(kThreads, 2)
               tmem_st32(tO + lane_off + cc * 32, o);
             }
           }
-          if (!kQT && g >= 2) wait_pv(g - 2);  // keep the observed phases contiguous (normally long complete)
+          if (g >= 2) wait_pv(g - 2);  // keep the observed phases contiguous (normally long complete)
           // P (bf16 pairs, low half = even key) over the first 32 columns of S buffer st
-          tmem_st32(s_col(g) + lane_off, pk);
+          tmem_st32(tmem + lane_off + st * kBN, pk);
           tmem_wait_st();
           tc_fence_before();
-          mbar_arrive(&bars[kQT ? B_P : B_P + st]);
+          mbar_arrive(&bars[B_P + st]);
           if (lane == 0) TRACE(T_SM_WARP_P + warp, g);
         }
         // epilogue: O / l -> bf16 -> global. Each warp stages its 32 rows x 32 dims
@@ -617,10 +543,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // apart, per instruction) took ~5000 cycles per item on the LSU path. A
         // warp whose rows run past the sequence end stores its valid rows directly
         // (a TMA box would overwrite the next sequence's rows).
-        if (kQT)
-          mbar_wait(&bars[B_O], it & 1);  // the item's last P.V (committed once per item)
-        else
-          wait_pv(gl);
+        wait_pv(gl);
         if (threadIdx.x == 0) TRACE(T_SM_EPI_PV, gl);
         tc_fence_after();
         const float inv_l = 1.f / l;
@@ -682,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           store_chunk(ob, 1);
         }
         tc_fence_before();
-        if (!kQT) mbar_arrive(&bars[B_OE]);  // the next item's first P.V may overwrite O (kQT: B_QT says so)
+        mbar_arrive(&bars[B_OE]);  // the next item's first P.V may overwrite O
         if (threadIdx.x == 0) TRACE(T_SM_EPI_DONE, gl);
       }
       g0 += ntiles;

@@ -27,6 +27,18 @@ __global__ void ex2h2_kernel(float *out, int iters, float seed) {
   for (int j = 0; j < 8; ++j) s ^= a[j];
   out[blockIdx.x * blockDim.x + threadIdx.x] = __uint_as_float(s);
 }
+__global__ void ex2bh2_kernel(float *out, int iters, float seed) {
+  // ex2.approx.ftz.bf16x2: two exponentials per lane per instruction
+  unsigned a[8];
+  for (int j = 0; j < 8; ++j) a[j] = 0xbc00bc00u + j + (unsigned)(seed * 16);
+  for (int i = 0; i < iters; ++i) {
+#define EB(x) asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(x));
+    EB(a[0]) EB(a[1]) EB(a[2]) EB(a[3]) EB(a[4]) EB(a[5]) EB(a[6]) EB(a[7])
+  }
+  unsigned s = 0;
+  for (int j = 0; j < 8; ++j) s ^= a[j];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = __uint_as_float(s);
+}
 __global__ void ffma_kernel(float *out, int iters, float seed) {
   float a0 = seed + threadIdx.x * 1e-6f, a1 = a0 + 0.1f, a2 = a0 + 0.2f, a3 = a0 + 0.3f;
   float a4 = a0 + 0.4f, a5 = a0 + 0.5f, a6 = a0 + 0.6f, a7 = a0 + 0.7f;
@@ -46,12 +58,13 @@ int main() {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int iters = 20000, blocks = sms * 4, threads = 512;
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < 4; ++k) {
     for (int w = 0; w < 2; ++w) {
       cudaEventRecord(e0);
       if (k == 0) ex2_kernel<<<blocks, threads>>>(out, iters, 0.5f);
       else if (k == 1) ffma_kernel<<<blocks, threads>>>(out, iters, 0.5f);
-      else ex2h2_kernel<<<blocks, threads>>>(out, iters, 0.5f);
+      else if (k == 2) ex2h2_kernel<<<blocks, threads>>>(out, iters, 0.5f);
+      else ex2bh2_kernel<<<blocks, threads>>>(out, iters, 0.5f);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
     }
@@ -60,7 +73,7 @@ int main() {
     double ops = double(blocks) * threads * iters * 8;
     double per_s = ops / (ms * 1e-3);
     // per SM per clock at the *current* clock is unknown; report per SM per ns and per clk at max clock
-    printf("%s: %.3f ms, %.1f Gop/s, %.2f op/clk/SM at max clock %d MHz\n", k == 0 ? "ex2.approx.f32" : k == 1 ? "ffma" : "ex2.approx.f16x2 (instr; x2 values)", ms,
+    printf("%s: %.3f ms, %.1f Gop/s, %.2f op/clk/SM at max clock %d MHz\n", k == 0 ? "ex2.approx.f32" : k == 1 ? "ffma" : k == 2 ? "ex2.approx.f16x2 (instr; x2 values)" : "ex2.approx.ftz.bf16x2 (instr; x2 values)", ms,
            per_s / 1e9, per_s / sms / (clk * 1e3), clk / 1000);
   }
   return 0;
