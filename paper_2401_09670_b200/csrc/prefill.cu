@@ -52,6 +52,25 @@ constexpr float kRescaleLog2 = 8.f;             // move the exponent base only p
 #endif
 constexpr int kPolyEvery = DS_PF_POLY_EVERY;    // 1 in kPolyEvery exp2 on the FMA pipe (ex2_poly)
 
+// Tail ordering. Launch order keeps a (sequence, head)'s q tiles together, heaviest
+// first, so their K/V re-reads hit L2 — but then the last groups' heavy tiles start
+// just before the end and the kernel ends on a tail (config 5, 8 x ~1.8k tokens x 24
+// heads: SM activity avg / max 0.90 under ncu). The LAST groups of the launch order
+// — as many as keep their K/V within DS_PF_BAND_MB of L2, at most kBandSeqs sequences
+// — are launched level-major instead: every band group's q tile i before any q tile
+// i-1 (tiles of a level by sequence length, descending, then head), so the heavy
+// tiles start first and the light ones fill the tail.
+#ifndef DS_PF_BAND_MB
+#define DS_PF_BAND_MB 48
+#endif
+constexpr int kBandSeqs = 32, kBandLevels = 64;
+struct Band {
+  int item0;   // first band item in launch order (n_loc * pref[num_seqs]: no band)
+  int levels;  // q-tile levels of the band (its longest sequence's tile count)
+  int seq[kBandSeqs], hlo[kBandSeqs];  // band sequences, tile count descending; first band head
+  int lvl[kBandLevels];                // band items of the levels above level i
+};
+
 template <int D>
 struct Smem {
   static constexpr uint32_t kQTile = kBM * D * 2;
@@ -61,7 +80,8 @@ struct Smem {
   static constexpr uint32_t V0 = K0 + 2 * kKVTile;     // 2 stages
   static constexpr uint32_t OST = V0 + 2 * kKVTile;    // epilogue staging: 4 warps x 32 rows x 32 dims bf16
   static constexpr uint32_t PREF = OST + 4 * 2048;     // int[kCompactSeqs + 1] tile prefix + 8 warp totals
-  static constexpr uint32_t CLC = PREF + (kCompactSeqs + 1 + 8) * 4 + 12;  // 2 x 16-B work-stealing responses
+  static constexpr uint32_t BAND = PREF + (kCompactSeqs + 1 + 8) * 4;  // struct Band (tail ordering)
+  static constexpr uint32_t CLC = (BAND + sizeof(Band) + 15) / 16 * 16;  // 2 x 16-B work-stealing responses
   static constexpr uint32_t BAR = CLC + 32;
   static constexpr uint32_t kBars = 21;
   static constexpr uint32_t TMEM_SLOT = BAR + kBars * 8;
@@ -132,7 +152,8 @@ enum { T_SM_WAIT_S = 1, T_SM_GOT_S, T_SM_P_DONE, T_MMA_S, T_MMA_WAIT_P, T_MMA_PV
 // costs a persistent CTA ~0.5 us to skip (64 x 128-token prompts launched with a
 // 2048-token bound: 85 -> 144 us). Items past the last tile come back as i = -1.
 // Without it (num_seqs > kCompactSeqs) the grid is num_q_tiles x n_loc x num_seqs.
-DS_DEVICE void item_coords(const PrefillArgs &a, const int *pref, int item, int &i, int &h, int &r) {
+DS_DEVICE void item_coords(const PrefillArgs &a, const int *pref, const Band &bd, int item, int &i, int &h,
+                           int &r) {
   if (!a.compact) {
     const int Q = a.num_q_tiles, g = item / Q;
     i = Q - 1 - (item - g * Q);
@@ -145,6 +166,25 @@ DS_DEVICE void item_coords(const PrefillArgs &a, const int *pref, int item, int 
     i = -1;
     r = h = 0;
     return;
+  }
+  if (item >= bd.item0) {  // the band: level-major (see Band)
+    int k = item - bd.item0, lo = 0, hi = bd.levels - 1;  // smallest level with lvl[level] <= k
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (bd.lvl[mid] <= k) hi = mid;
+      else lo = mid + 1;
+    }
+    i = lo;
+    k -= bd.lvl[lo];
+    for (int s = 0;; ++s) {  // the level's sequences are a prefix of the length-sorted band
+      const int hs = n - bd.hlo[s];
+      if (k < hs) {
+        r = bd.seq[s];
+        h = bd.hlo[s] + k;
+        return;
+      }
+      k -= hs;
+    }
   }
   int lo = 0, hi = a.num_seqs - 1;  // largest r with n * pref[r] <= item
   while (lo < hi) {
@@ -182,6 +222,69 @@ DS_DEVICE void build_tile_prefix(const PrefillArgs &a, int *pref, int *warp_tot)
     run += (a.cu_seqlens[b + 1] - a.cu_seqlens[b] + kBM - 1) / kBM;
   }
   if (t == kThreads - 1) pref[B] = base + inc;
+}
+
+// The band (see Band), by one warp once pref is complete: lane t looks at sequence
+// num_seqs-1-t; the band takes whole sequences from the end (and the last heads of one
+// more) while their K/V bytes fit the budget; ranks by tile count sort them; level
+// counts and their suffix sums give lvl.
+DS_DEVICE void build_band(const PrefillArgs &a, const int *pref, Band &bd, int head_dim) {
+  const int B = a.num_seqs, n = a.n_loc, lane = threadIdx.x & 31, r = B - 1 - lane;
+  const int64_t per_token = 4LL * head_dim;  // K + V bytes of one head
+  const int len = r >= 0 ? a.cu_seqlens[r + 1] - a.cu_seqlens[r] : 0;
+  const int tr = r >= 0 ? pref[r + 1] - pref[r] : 0;
+  const int64_t sb = (int64_t)n * len * per_token;
+  int64_t inc = sb;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  const int64_t budget = (int64_t)DS_PF_BAND_MB << 20, before = inc - sb;
+  int heads = 0;
+  if (r >= 0 && len > 0 && before < budget) heads = (int)min((int64_t)n, (budget - before) / (len * per_token));
+  const unsigned in = __ballot_sync(0xffffffffu, heads > 0);  // a prefix of the lanes
+  const int nseq = in == 0xffffffffu ? 32 : __ffs(~in) - 1;
+  int levels = heads > 0 ? tr : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) levels = max(levels, __shfl_xor_sync(0xffffffffu, levels, o));
+  if (nseq == 0 || levels > kBandLevels) {
+    if (lane == 0) {
+      bd.item0 = n * pref[B];
+      bd.levels = 0;
+    }
+    return;
+  }
+  int rank = 0, items = heads * tr, cnt_lo = 0, cnt_hi = 0;
+  for (int t = 0; t < nseq; ++t) {
+    const int tr_t = __shfl_sync(0xffffffffu, tr, t), h_t = __shfl_sync(0xffffffffu, heads, t);
+    if (tr_t > tr || (tr_t == tr && t > lane)) ++rank;  // longer first; ties in launch order
+    if (tr_t > lane) cnt_lo += h_t;                      // items of level `lane`
+    if (tr_t > lane + 32) cnt_hi += h_t;                 // items of level `lane + 32`
+  }
+  if (lane < nseq) {
+    bd.seq[rank] = r;
+    bd.hlo[rank] = n - heads;
+  }
+  // lvl[i] = sum of the level counts above i (suffix sums over lanes, hi levels first)
+  int suf_hi = cnt_hi, suf_lo = cnt_lo;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int yh = __shfl_down_sync(0xffffffffu, suf_hi, o), yl = __shfl_down_sync(0xffffffffu, suf_lo, o);
+    if (lane + o < 32) {
+      suf_hi += yh;
+      suf_lo += yl;
+    }
+  }
+  const int tot_hi = __shfl_sync(0xffffffffu, suf_hi, 0);
+  bd.lvl[lane + 32] = suf_hi - cnt_hi;
+  bd.lvl[lane] = suf_lo - cnt_lo + tot_hi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) items += __shfl_xor_sync(0xffffffffu, items, o);
+  if (lane == 0) {
+    bd.item0 = n * pref[B] - items;
+    bd.levels = levels;
+  }
 }
 
 // waits of the producer and MMA threads
@@ -224,7 +327,18 @@ __global__ void __launch_bounds__(kThreads, 2)
     tmem_relinquish();
   }
   int *pref = reinterpret_cast<int *>(smem + S::PREF);
-  if (a.compact) build_tile_prefix(a, pref, pref + kCompactSeqs + 1);
+  Band &band = *reinterpret_cast<Band *>(smem + S::BAND);
+  if (a.compact) {
+    build_tile_prefix(a, pref, pref + kCompactSeqs + 1);
+    __syncthreads();
+    // (prompts of at most 2 q tiles have no heavy items to reorder: skip the band)
+    if (warp == 0) {
+      if (a.num_q_tiles > 2)
+        build_band(a, pref, band, D);
+      else if (lane == 0)
+        band.item0 = a.n_loc * pref[a.num_seqs];
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -267,7 +381,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       clc_try_cancel(sbase + S::CLC + (q & 1) * 16, &bars[B_CLC + (q & 1)]);
     }
     int i, h, r;
-    item_coords(a, pref, item, i, h, r);
+    item_coords(a, pref, band, item, i, h, r);
     const int seq_start = a.cu_seqlens[r];
     const int len = a.cu_seqlens[r + 1] - seq_start;
     if (i >= 0 && i * kBM < len) {
@@ -568,7 +682,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             v[u] = make_uint4(w[0], w[1], w[2], w[3]);
           }
           if (boxed) {
-            // (a second staging buffer per warp measured no faster)
+            // (a second staging buffer per warp measured no faster; per-thread 32-B
+            // STG.256 row stores 1-5 % slower, profiles/r02/prefill_band_ab)
             if (lane == 0) bulk_wait_group_read0();  // the previous chunk's store has read the buffer
             __syncwarp();
 #pragma unroll
