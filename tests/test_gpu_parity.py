@@ -147,6 +147,36 @@ def test_prefill_full_size_config2_sampled(oracle_mod):
     assert not np.isnan(got).any()
 
 
+def test_prefill_tail_band_partial_sequence_sampled(oracle_mod):
+    """The tail band (prefill.cu, Band: the last groups whose K/V fit 48 MiB run
+    level-major): 16 heads x [3000, 1000, 4000, 2000] tokens puts the whole of
+    sequences 3 and 2 and the last 2 heads of sequence 1 in the band (32 + 16 + 8
+    q-tile levels). Two rows of EVERY (sequence, head, q tile) — a random one and the
+    tile's last row — against the oracle, and every page written."""
+    lens, n, d = [3000, 1000, 4000, 2000], 16, 128
+    g = syn.rng(21)
+    rows = []
+    for r, l in enumerate(lens):
+        for h in range(n):
+            for i in range(_ceil(l, 128)):
+                hi = min(l, 128 * (i + 1))
+                rows += [(r, int(g.integers(128 * i, hi)), h), (r, hi - 1, h)]
+    _, side, table, got, err = run_prefill(oracle_mod, lens, n, d, seed=21, full_check=False, sample_rows=rows)
+    assert err <= TOL and err <= WARN_PREFILL, err
+    assert not np.isnan(got).any()
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, lens, table)
+
+
+def test_prefill_tail_band_sequence_cap_full(oracle_mod):
+    """40 sequences of 300 tokens (3 q tiles) x 8 heads all fit the band's byte
+    budget; the band stops at its 32-sequence cap (sequences 8..39 level-major, 0..7
+    in the plain order). Full oracle comparison."""
+    lens = [300 - (r % 5) for r in range(40)]
+    b, side, table, got, err = run_prefill(oracle_mod, lens, 8, 128, seed=22)
+    assert err <= TOL and err <= WARN_PREFILL, err
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, lens, table)
+
+
 def test_bench_step_shape_fused_prefill_then_dynamic_decode(oracle_mod):
     """The bench's default launch configuration (config 2: OPT-13B heads, 128 x 512-token
     prompts): the fused prefill+migration into the decode pool (sampled output rows vs
