@@ -10,4 +10,5 @@ cp -r "$ROOT/include" "$d/"
 mkdir -p "$d/paper_2401_09670_b200"
 cp -r "$ROOT/paper_2401_09670_b200/csrc" "$ROOT/paper_2401_09670_b200/"*.py "$d/paper_2401_09670_b200/"
 DS_NVCC_DEFS="$2" python "$d/paper_2401_09670_b200/build.py" --force >/dev/null
+rm -rf "$d/paper_2401_09670_b200/_build"  # objects are not needed at run time (smaller gpurun pushes)
 echo "$d"
