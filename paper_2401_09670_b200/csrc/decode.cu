@@ -61,18 +61,6 @@ constexpr int kChunkPages = DS_DEC_CHUNK;
 #define DS_DEC_DYN_MINPW 64
 #endif
 constexpr int kDynMinPagesPerWarp = DS_DEC_DYN_MINPW;
-// Two-tier dynamic chunks (A/B): the last kTailPct % of the dynamic pages are cut
-// into chunks of kTailChunk pages, so the warps that take the last chunks finish
-// closer together (an 8-page chunk streams for ~8-10 us on one warp).
-#ifndef DS_DEC_TAIL_PCT
-#define DS_DEC_TAIL_PCT 0
-#endif
-#ifndef DS_DEC_TAIL_CHUNK
-#define DS_DEC_TAIL_CHUNK 2
-#endif
-constexpr int kTailPct = DS_DEC_TAIL_PCT;
-constexpr int kTailChunk = DS_DEC_TAIL_CHUNK;
-static_assert(kChunkPages % kTailChunk == 0, "tail chunks tile the 8-page grid");
 constexpr int kRangeQ = 4;  // range queue entries per warp (the producer is < 2 pages ahead)
 constexpr int kMaxSeqs = kDecodeMaxSeqs;
 constexpr float kNegInf = -__builtin_huge_valf();
@@ -203,37 +191,27 @@ DS_DEVICE int64_t owner_of(int64_t x, int64_t W, int64_t P) {
 // contiguous, non-empty and in page order, so a (seq, head) pair's contributors
 // are the consecutive virtual workers owning its first .. last page.
 struct Part {
-  int64_t W, P1, P, NC;  // static warps, end of the static pages, pages, dynamic chunks
-  int64_t NC8, P2;       // chunks of kChunkPages (over [P1, P2)); then kTailChunk-page ones
+  int64_t W, P1, P, NC;
 };
 __host__ __device__ inline Part make_part(int64_t P, int64_t Wmax, int64_t max_chunks) {
   Part q;
   q.W = P < Wmax ? P : Wmax;
-  int64_t dyn = 0, dyn2 = 0;
+  int64_t dyn = 0;
   // only with >= 64 pages per warp (measured: B = 128 and 256 x 544 tokens gain 5-7 %,
   // B <= 64 loses up to 10 %: there the takes, the chunk partials and their merges
   // cost more than the balance gains)
   if (kDynPct > 0 && P >= kDynMinPagesPerWarp * q.W) dyn = (P * kDynPct / 100) / kChunkPages * kChunkPages;
-  if (kTailPct > 0) dyn2 = (dyn * kTailPct / 100) / kChunkPages * kChunkPages;
-  if ((dyn - dyn2) / kChunkPages + dyn2 / kTailChunk > max_chunks) {  // workspace bound: one tier
-    dyn2 = 0;
-    if (dyn > max_chunks * kChunkPages) dyn = max_chunks * kChunkPages;
-  }
+  if (dyn > max_chunks * kChunkPages) dyn = max_chunks * kChunkPages;  // workspace bound
   q.P1 = P - dyn;
   q.P = P;
-  q.NC8 = (dyn - dyn2) / kChunkPages;
-  q.P2 = q.P1 + q.NC8 * kChunkPages;
-  q.NC = q.NC8 + dyn2 / kTailChunk;
+  q.NC = dyn / kChunkPages;
   return q;
 }
-__host__ __device__ inline int64_t vbegin(const Part &q, int64_t v) {
-  if (v <= q.W) return range_begin(v, q.W, q.P1);
-  const int64_t c = v - q.W;
-  return c <= q.NC8 ? q.P1 + c * kChunkPages : q.P2 + (c - q.NC8) * kTailChunk;
+DS_DEVICE int64_t vbegin(const Part &q, int64_t v) {
+  return v <= q.W ? range_begin(v, q.W, q.P1) : q.P1 + (v - q.W) * kChunkPages;
 }
 DS_DEVICE int64_t vowner(const Part &q, int64_t x) {
-  if (x < q.P1) return owner_of(x, q.W, q.P1);
-  return x < q.P2 ? q.W + (x - q.P1) / kChunkPages : q.W + q.NC8 + (x - q.P2) / kTailChunk;
+  return x < q.P1 ? owner_of(x, q.W, q.P1) : q.W + (x - q.P1) / kChunkPages;
 }
 
 // partial row of warp w, segment seg (0: its first pair, 1: its last pair):
@@ -699,7 +677,7 @@ DecodeLayout decode_layout(int num_seqs, int n_loc, int head_dim, int num_sms, i
   L.rows_off = L.tickets_off + (size_t)kDecodeMaxPairs * 4;
   L.chunk_off = L.rows_off + (size_t)num_sms * kWarps * 2 * row;
   const int64_t pmax = (int64_t)num_seqs * n_loc * npages_of(max_cache_len);
-  const Part q = make_part(pmax, (int64_t)num_sms * kWarps, INT64_MAX / 2);
+  const Part q = make_part(pmax, (int64_t)num_sms * kWarps, INT64_MAX / kChunkPages);
   L.max_chunks = q.NC;
   L.total = L.chunk_off + (size_t)q.NC * 2 * row;
   return L;
