@@ -44,7 +44,12 @@ namespace {
 #ifndef DS_DEC_SLOTS
 #define DS_DEC_SLOTS 3
 #endif
-constexpr int kWarps = DS_DEC_WARPS;  // consumer warps per CTA (one CTA per SM)
+#ifndef DS_DEC_CTAS
+#define DS_DEC_CTAS 1
+#endif
+constexpr int kWarps = DS_DEC_WARPS;           // consumer warps per CTA
+constexpr int kCtasPerSm = DS_DEC_CTAS;        // resident CTAs per SM (A/B: 2 x 8 warps)
+constexpr int kWarpsPerSm = kWarps * kCtasPerSm;
 #ifndef DS_DEC_DYN_PCT
 #define DS_DEC_DYN_PCT 10
 #endif
@@ -61,7 +66,9 @@ constexpr int kChunkPages = DS_DEC_CHUNK;
 #define DS_DEC_DYN_MINPW 64
 #endif
 constexpr int kDynMinPagesPerWarp = DS_DEC_DYN_MINPW;
-constexpr int kRangeQ = 4;  // range queue entries per warp (the producer is < 2 pages ahead)
+// range queue entries per warp (the producer is < 2 pages ahead, so 2 would do; 3 lets
+// two 8-warp CTAs fit one SM's 228 KiB)
+constexpr int kRangeQ = kCtasPerSm > 1 ? 3 : 4;
 constexpr int kMaxSeqs = kDecodeMaxSeqs;
 constexpr float kNegInf = -__builtin_huge_valf();
 
@@ -377,7 +384,7 @@ DS_DEVICE void consume_page(const uint8_t *kst, const uint8_t *vst, const uint4 
 #ifdef DS_TRACE
 // per-warp globaltimer stamps (A/B trace builds only): entry, prefix built, first
 // page ready, loop done; read back with ds_debug_decode_trace
-__device__ unsigned long long g_dec_trace[kDecodeMaxSMs * kWarps][6];
+__device__ unsigned long long g_dec_trace[kDecodeMaxSMs * kWarpsPerSm][6];
 DS_DEVICE unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -393,7 +400,7 @@ DS_DEVICE unsigned long long gtimer() {
 // reach >= 64 pages per warp); the static-only instance keeps the short path of
 // small batches free of the range queue (measured 1-3 us per launch at B <= 32).
 template <int D, bool kDyn>
-__global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const DecodeArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) decode_kernel(const DecodeArgs a) {
   using C = DecCfg<D>;
   constexpr int TPG = D / 8;  // lanes per token row
   extern __shared__ __align__(128) uint8_t smem[];
@@ -675,9 +682,9 @@ DecodeLayout decode_layout(int num_seqs, int n_loc, int head_dim, int num_sms, i
   L.dyn_off = 0;
   L.tickets_off = 16;
   L.rows_off = L.tickets_off + (size_t)kDecodeMaxPairs * 4;
-  L.chunk_off = L.rows_off + (size_t)num_sms * kWarps * 2 * row;
+  L.chunk_off = L.rows_off + (size_t)num_sms * kWarpsPerSm * 2 * row;
   const int64_t pmax = (int64_t)num_seqs * n_loc * npages_of(max_cache_len);
-  const Part q = make_part(pmax, (int64_t)num_sms * kWarps, INT64_MAX / kChunkPages);
+  const Part q = make_part(pmax, (int64_t)num_sms * kWarpsPerSm, INT64_MAX / kChunkPages);
   L.max_chunks = q.NC;
   L.total = L.chunk_off + (size_t)q.NC * 2 * row;
   return L;
@@ -701,7 +708,7 @@ static cudaError_t launch_d(cudaLaunchConfig_t &cfg, const DecodeArgs &a) {
 
 cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaStream_t stream) {
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(num_sms);
+  cfg.gridDim = dim3(num_sms * kCtasPerSm);
   cfg.blockDim = dim3(kWarps * 32);
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
@@ -712,7 +719,7 @@ cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaSt
   // dynamic chunks only if the batch can reach the threshold (an upper bound of the
   // page count from max_cache_len; the kernel decides exactly from the lengths)
   const int64_t pmax = (int64_t)a.num_seqs * a.n_loc * npages_of(a.max_cache_len);
-  const bool dyn = a.max_chunks > 0 && make_part(pmax, (int64_t)num_sms * kWarps, a.max_chunks).NC > 0;
+  const bool dyn = a.max_chunks > 0 && make_part(pmax, (int64_t)num_sms * kWarpsPerSm, a.max_chunks).NC > 0;
   cudaError_t e;
   if (head_dim == 128)
     e = dyn ? launch_d<128, true>(cfg, a) : launch_d<128, false>(cfg, a);
