@@ -371,6 +371,40 @@ def test_decode_batch256_config3_shape_sampled(oracle_mod):
     assert max(errs) <= WARN, errs
 
 
+def test_config5_shape_prefill_and_decode_sampled(oracle_mod):
+    """BASELINE config 5 as bench.py --config 5 launches it on one GPU: OPT-175B heads
+    (96 x 128), the LongBench-like summarization mix (8 prompts, 737-1878 tokens). The
+    prefill (tail band active: 96 heads x 1.9k tokens exceed its budget) on sampled rows
+    of every sequence and every page of three heads; then one decode step over the
+    8 x 96 pairs at decode-snapshot contexts (input + U[0, output)) against the oracle."""
+    inp, out = syn.lengths_summarization(0, 8)
+    lens, n = [int(x) for x in inp], 96
+    g = syn.rng(55)
+    rows = [(r, int(i), int(g.integers(n))) for r, l in enumerate(lens) for i in g.integers(0, l, 24)]
+    rows += [(r, l - 1, h) for r, l in enumerate(lens) for h in (0, n - 1)]
+    _, side, table, got, err = run_prefill(oracle_mod, lens, n, 128, seed=55, full_check=False, sample_rows=rows)
+    assert err <= TOL and err <= WARN_PREFILL, err
+    assert not np.isnan(got).any()
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, lens, table, heads=[0, 47, 95])
+    ctx = [int(x) for x in syn.decode_snapshot_contexts(5, inp, out)]
+    _, _, _, errs = run_decode(oracle_mod, ctx, n, 128, seed=56, steps=1)
+    assert max(errs) <= WARN, errs
+
+
+def test_config4_shape_prefill_and_decode(oracle_mod):
+    """BASELINE config 4 as bench.py --config 4 launches it on one GPU: OPT-66B heads
+    (72 x 128), the HumanEval-like code mix (32 prompts of 32-512 tokens): the whole
+    prefill against the oracle, then two decode steps over the 32 x 72 pairs."""
+    inp, out = syn.lengths_code(0, 164)
+    lens = [int(x) for x in inp[:32]]
+    _, side, table, got, err = run_prefill(oracle_mod, lens, 72, 128, seed=57)
+    assert err <= TOL and err <= WARN_PREFILL, err
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, lens, table, heads=[0, 35, 71])
+    ctx = [int(x) for x in syn.decode_snapshot_contexts(6, inp[:32], out[:32])]
+    _, _, _, errs = run_decode(oracle_mod, ctx, 72, 128, seed=58, steps=2)
+    assert max(errs) <= WARN, errs
+
+
 def _decode_layer_chain(oracle_mod, ctx, n, d, layers, seed, early, graph):
     """Prefill `layers` layers of one pool, then one decode step over every layer,
     back to back on one stream (optionally as one CUDA graph, whose PDL edges let
