@@ -103,15 +103,13 @@ static ds_status qkv_map(CUtensorMap *m, const void *p, int T, int n, int D, int
   return encode(m, const_cast<void *>(p), 3, dims, str, box, where);
 }
 
-// prefill output [T][n][D]: box = 32 tokens x `box_dims` (32 or 16) dims of one head,
-// 64-B (32-B) swizzle (the epilogue of one softmax warp: its 32 q rows, one 32-column
-// TMEM chunk — or half of one — at a time)
-static ds_status out_map(CUtensorMap *m, void *p, int T, int n, int D, const char *where, int box_dims = 32) {
+// prefill output [T][n][D]: box = 32 tokens x 32 dims of one head, 64-B swizzle (the
+// epilogue of one softmax warp: its 32 q rows, one 32-column TMEM chunk at a time)
+static ds_status out_map(CUtensorMap *m, void *p, int T, int n, int D, const char *where) {
   const cuuint64_t dims[3] = {(cuuint64_t)D, (cuuint64_t)n, (cuuint64_t)T};
   const cuuint64_t str[2] = {(cuuint64_t)D * 2, (cuuint64_t)n * D * 2};
-  const cuuint32_t box[3] = {(cuuint32_t)box_dims, 1, 32};
-  return encode(m, p, 3, dims, str, box, where,
-                box_dims == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_64B);
+  const cuuint32_t box[3] = {32, 1, 32};
+  return encode(m, p, 3, dims, str, box, where, CU_TENSOR_MAP_SWIZZLE_64B);
 }
 
 // pool [L*2*NB][n][16][D]; box = one 16-token page x 64 dims
@@ -187,7 +185,7 @@ static ds_status prefill_impl(const char *W, const void *q, const void *k, const
   const int kv_rows = two_q ? 128 : kPrefillKVRows;
   CUtensorMap tq, tk, tv, tc, to, tdst;
   if (ds_status s = qkv_map(&tq, q, total_tokens, n, D, kPrefillQRows, W)) return s;
-  if (ds_status s = out_map(&to, out, total_tokens, n, D, W, two_q ? 32 : kPrefillOutBoxDims)) return s;
+  if (ds_status s = out_map(&to, out, total_tokens, n, D, W)) return s;
   if (ds_status s = qkv_map(&tk, k, total_tokens, n, D, kv_rows, W)) return s;
   if (ds_status s = qkv_map(&tv, v, total_tokens, n, D, kv_rows, W)) return s;
   if (ds_status s = cache_map(&tc, cache, W)) return s;
@@ -271,7 +269,7 @@ extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const
   const int D = cache->head_dim, n = cache->num_heads;
   CUtensorMap tq, tk, tv, tc, to;
   if (ds_status s = qkv_map(&tq, q, total_tokens, n, D, kPrefillQRows, W)) return s;
-  if (ds_status s = out_map(&to, out, total_tokens, n, D, W, kPrefillOutBoxDims)) return s;
+  if (ds_status s = out_map(&to, out, total_tokens, n, D, W)) return s;
   if (ds_status s = qkv_map(&tk, k, total_tokens, n, D, kPrefillKVRows, W)) return s;
   if (ds_status s = qkv_map(&tv, v, total_tokens, n, D, kPrefillKVRows, W)) return s;
   if (ds_status s = cache_map(&tc, cache, W)) return s;

@@ -62,10 +62,6 @@ cudaError_t launch_kv_local(const KvLocalArgs &a, cudaStream_t stream);
 // a2 + a3
 constexpr int kPrefillQRows = 128;  // q rows per CTA (TMA box of Q)
 constexpr int kPrefillKVRows = 64;  // keys per kv tile (TMA box of K and V)
-#ifndef DS_PF_EPI16  // A/B: O stored in 16-dim boxes (double-buffered staging) instead of 32
-#define DS_PF_EPI16 0
-#endif
-constexpr int kPrefillOutBoxDims = DS_PF_EPI16 ? 16 : 32;  // dims per O store box
 struct PrefillArgs {
   void *out;                   // bf16 [T][n][D]
   const int32_t *cu_seqlens;   // [B+1]

@@ -51,11 +51,6 @@ constexpr float kRescaleLog2 = 8.f;             // move the exponent base only p
 #define DS_PF_SLEEP_NS 0
 #endif
 constexpr int kPolyEvery = DS_PF_POLY_EVERY;    // 1 in kPolyEvery exp2 on the FMA pipe (ex2_poly)
-constexpr int kOutBox = kPrefillOutBoxDims;     // dims per O store box (api.cu's out_map)
-#ifndef DS_PF_STORE_GROUPS  // A/B: the paged K/V stores of each diagonal tile as their own bulk group
-#define DS_PF_STORE_GROUPS 0
-#endif
-constexpr bool kStoreGroups = DS_PF_STORE_GROUPS != 0;
 
 // Tail ordering. Launch order keeps a (sequence, head)'s q tiles together, heaviest
 // first, so their K/V re-reads hit L2 — but then the last groups' heavy tiles start
@@ -408,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
           for (int c = 0; c < kChunks; ++c)
             tma_load_3d(smem + S::Q + c * kChunkBytes128, &tm_q, &bars[B_Q], c * 64, h, seq_start + i * kBM);
-          if (store_pending && !kStoreGroups) {  // the previous item's paged stores read the stages we refill now
+          if (store_pending) {  // the previous item's paged stores read the stages we refill now
             bulk_wait_group_read0();
             store_pending = false;
           }
@@ -438,16 +433,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                                 (a.layer * 2 + kv) * a.num_blocks + btr[p0 + min(p, np - 1)]);
               }
               continue;
-            }
-            if (kStoreGroups && store_pending) {
-              // one store group per diagonal tile of the previous item: its newest group
-              // reads the stage of its last tile, which the first tile here does not use
-              if (j == 0) {
-                bulk_wait_group_read1();
-              } else {
-                bulk_wait_group_read0();
-                store_pending = false;
-              }
             }
             const int kv0 = seq_start + (j - npt) * kBN;
             if (g >= 2) ctl_wait(&bars[B_KE + st], ph_free);  // S_{g-2} has consumed the K stage
@@ -492,10 +477,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                                  (a.dst_layer * 2 + kv) * a.dst_num_blocks + dblk);
                 }
             }
-            if (kStoreGroups) bulk_commit_group();  // one group per diagonal tile (stage)
           }
           if (npg > 0) {
-            if (!kStoreGroups) bulk_commit_group();
+            bulk_commit_group();
             store_pending = true;
           }
         }
@@ -697,26 +681,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             v[u] = make_uint4(w[0], w[1], w[2], w[3]);
           }
-          if (kOutBox == 16 && boxed) {
-            // A/B: two 16-dim boxes per 32-column chunk, alternating between two 1-KiB
-            // halves of the warp's staging buffer (32-B swizzle: conflict-free STS), so
-            // a half is reused only once the store before the previous one has read it
-#pragma unroll
-            for (int hb = 0; hb < 2; ++hb) {
-              uint8_t *buf = stg + hb * 1024;
-              if (lane == 0) bulk_wait_group_read1();
-              __syncwarp();
-#pragma unroll
-              for (int u = 0; u < 2; ++u)
-                *reinterpret_cast<uint4 *>(buf + lane * 32 + ((u ^ ((lane >> 2) & 1)) << 4)) = v[2 * hb + u];
-              fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                tma_store_3d(&tm_o, buf, cc * 32 + hb * 16, h, seq_start + row0);
-                bulk_commit_group();
-              }
-            }
-          } else if (boxed) {
+          if (boxed) {
             // (a second staging buffer per warp measured no faster; per-thread 32-B
             // STG.256 row stores 1-5 % slower, profiles/r02/prefill_band_ab)
             if (lane == 0) bulk_wait_group_read0();  // the previous chunk's store has read the buffer
