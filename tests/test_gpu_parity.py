@@ -371,6 +371,22 @@ def test_decode_batch256_config3_shape_sampled(oracle_mod):
     assert max(errs) <= WARN, errs
 
 
+def test_prefill_long_prompt_band_disabled_sampled(oracle_mod):
+    """A 9000-token prompt has 71 q-tile levels, more than the band's 64: the band is
+    off and the plain launch order runs (plus a short sequence). Sampled rows of every
+    q tile of both sequences and heads against the oracle; every page."""
+    lens, n = [9000, 300], 2
+    g = syn.rng(23)
+    rows = []
+    for r, l in enumerate(lens):
+        for h in range(n):
+            for i in range(_ceil(l, 128)):
+                rows.append((r, int(g.integers(128 * i, min(l, 128 * (i + 1)))), h))
+    _, side, table, got, err = run_prefill(oracle_mod, lens, n, 128, seed=23, full_check=False, sample_rows=rows)
+    assert err <= TOL and err <= WARN_PREFILL, err
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, lens, table)
+
+
 def test_config5_shape_prefill_and_decode_sampled(oracle_mod):
     """BASELINE config 5 as bench.py --config 5 launches it on one GPU: OPT-175B heads
     (96 x 128), the LongBench-like summarization mix (8 prompts, 737-1878 tokens). The
