@@ -1019,6 +1019,8 @@ def run_ds(args):
     eng.push_drain()
     if world > 1 and args.transport != "push":  # push: the migration is inside the prefill kernel
         comp.update(measure_migration(eng, w, world, torch))
+    elif world == 1 and eng.transport == "local":
+        comp.update(measure_local_migration(eng, w, torch))
     if not args.no_e2e:
         line["e2e"] = run_e2e(args, eng, w, world, replicas, torch)
         eng.pull_drain()
@@ -1105,6 +1107,36 @@ def measure_migration(eng, w, world, torch, reps=3):
     gbps = reps * nb * w.kv_page_bytes() / (ms / 1e3) / 1e9
     return {"kv_migrate_isolated_GBps": gbps, "kv_migrate_isolated_frac_of_nvlink": gbps / NVLINK_GBS,
             "kv_migrate_isolated_ms_per_batch": ms / (reps * nb)}
+
+
+def measure_local_migration(eng, w, torch, reps=3):
+    """N=1: the one-GPU step fuses the migration into the prefill kernel (no pass of its
+    own); this times the separate LOCAL page copy (ds_kv_migrate LOCAL, prefill pool ->
+    decode pool, one batch, all layers) alone, for the migrate metric at one GPU."""
+    ds, peaks = eng.ds, load_peaks()[0]
+    tp = np.full((w.B, w.maxb), -1, np.int32)
+    ds.ds_block_table(eng.pool_p, ds.DS_BT_APPEND, [0] * w.B, w.lens, tp)
+    src_ids = eng.page_ids(eng.upload(tp))
+    eng.admit()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ds.ds_kv_migrate(None, ds.DS_MIGRATE_LOCAL, 0, eng.P, 0, w.L, src_ids, 0, w.n, None, dst_cache=eng.D,
+                     dst_block_ids=eng.dst_ids)  # warm-up
+    e0.record()
+    for _ in range(reps):
+        ds.ds_kv_migrate(None, ds.DS_MIGRATE_LOCAL, 0, eng.P, 0, w.L, src_ids, 0, w.n, None, dst_cache=eng.D,
+                         dst_block_ids=eng.dst_ids)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    ds.ds_block_table(eng.pool_p, ds.DS_BT_FREE, w.lens, None, tp)
+    ds.ds_block_table(eng.pool_d, ds.DS_BT_FREE, w.lens, None, eng.td)
+    gbps = w.kv_page_bytes() / (ms / 1e3) / 1e9
+    return {"kv_migrate_local_GBps": gbps, "kv_migrate_local_ms_per_batch": ms,
+            "kv_migrate_local_frac_of_hbm": 2 * gbps / peaks["hbm_gbs"],
+            "kv_migrate_local_note": "one-GPU LOCAL page copy (prefill pool -> decode pool) timed alone; reads and "
+                                     "writes each page once, so its HBM roofline is 2 x bytes / copy peak; the "
+                                     "bench step itself fuses the migration into the prefill kernel"}
 
 
 def run_e2e(args, eng, w, world, replicas, torch):
