@@ -226,14 +226,16 @@ DS_DEVICE void build_tile_prefix(const PrefillArgs &a, int *pref, int *warp_tot)
 
 // The band (see Band), by one warp once pref is complete: lane t looks at sequence
 // num_seqs-1-t; the band takes whole sequences from the end (and the last heads of one
-// more) while their K/V bytes fit the budget; ranks by tile count sort them; level
-// counts and their suffix sums give lvl.
+// more) while their K/V bytes (chunked prefill: with the cached prefix) fit the
+// budget; ranks by tile count sort them; level counts and their suffix sums give lvl.
 DS_DEVICE void build_band(const PrefillArgs &a, const int *pref, Band &bd, int head_dim) {
   const int B = a.num_seqs, n = a.n_loc, lane = threadIdx.x & 31, r = B - 1 - lane;
   const int64_t per_token = 4LL * head_dim;  // K + V bytes of one head
   const int len = r >= 0 ? a.cu_seqlens[r + 1] - a.cu_seqlens[r] : 0;
   const int tr = r >= 0 ? pref[r + 1] - pref[r] : 0;
-  const int64_t sb = (int64_t)n * len * per_token;
+  // K/V a group re-reads: its own tokens, plus the cached prefix in chunked prefill
+  const int64_t kv_len = len + (r >= 0 && a.prefix_lens ? a.prefix_lens[r] : 0);
+  const int64_t sb = (int64_t)n * kv_len * per_token;
   int64_t inc = sb;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -242,7 +244,7 @@ DS_DEVICE void build_band(const PrefillArgs &a, const int *pref, Band &bd, int h
   }
   const int64_t budget = (int64_t)DS_PF_BAND_MB << 20, before = inc - sb;
   int heads = 0;
-  if (r >= 0 && len > 0 && before < budget) heads = (int)min((int64_t)n, (budget - before) / (len * per_token));
+  if (r >= 0 && len > 0 && before < budget) heads = (int)min((int64_t)n, (budget - before) / (kv_len * per_token));
   const unsigned in = __ballot_sync(0xffffffffu, heads > 0);  // a prefix of the lanes
   const int nseq = in == 0xffffffffu ? 32 : __ffs(~in) - 1;
   int levels = heads > 0 ? tr : 0;
