@@ -312,7 +312,7 @@ def test_decode_dynamic_chunks(oracle_mod):
     first: results must not depend on who took what (two launches: oracle parity
     and pages each time), and the self-resetting chunk counters must be ready for
     the next launch (the second decode step reuses the workspace)."""
-    ctx = [int(x) for x in syn.rng(21).integers(300, 900, 512)]
+    ctx = [int(x) for x in syn.rng(21).integers(200, 500, 512)]  # 181k pages: >= 64 per warp of 2368
     side, table, cur, errs = run_decode(oracle_mod, ctx, 16, 128, seed=21, steps=2)
     assert max(errs) <= WARN, errs
     assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
@@ -323,7 +323,7 @@ def test_decode_dynamic_chunks_ragged_d64(oracle_mod):
     one-page and many-page sequences, so chunks start and end inside pairs, cover
     whole short pairs, and cross sequence boundaries."""
     g = syn.rng(22)
-    ctx = [int(x) for x in g.integers(0, 1200, 700)]
+    ctx = [int(x) for x in g.integers(0, 600, 700)]
     ctx[:40] = [0] * 10 + [1] * 10 + [15] * 10 + [16] * 10
     side, table, cur, errs = run_decode(oracle_mod, ctx, 24, 64, seed=22, steps=2, fragment=7)
     assert max(errs) <= WARN, errs
@@ -338,11 +338,11 @@ def test_decode_workspace_reused_across_batch_shapes(oracle_mod):
     region, so no call finds them on top of an earlier call's partial rows."""
     g = syn.rng(31)
     calls = [
-        ([int(x) for x in g.integers(300, 900, 512)], 16, 128),   # dynamic tail
-        ([int(x) for x in g.integers(300, 900, 700)], 24, 128),   # more pairs, dynamic tail
+        ([int(x) for x in g.integers(200, 500, 512)], 16, 128),   # dynamic tail (>= 64 pages per warp)
+        ([int(x) for x in g.integers(150, 400, 700)], 24, 128),   # more pairs, dynamic tail
         ([int(x) for x in g.integers(0, 700, 96)], 8, 64),        # another head_dim
-        ([int(x) for x in g.integers(300, 1200, 600)], 24, 64),   # dynamic tail at head_dim 64
-        ([int(x) for x in g.integers(300, 900, 512)], 16, 128),   # the first shape again
+        ([int(x) for x in g.integers(200, 500, 600)], 24, 64),    # dynamic tail at head_dim 64
+        ([int(x) for x in g.integers(200, 500, 512)], 16, 128),   # the first shape again
     ]
     need = max(ds.ds_decode_workspace_bytes(len(c), n, d, max(c) + 2) for c, n, d in calls)
     ws = torch.zeros(need // 4 + 4, dtype=torch.float32, device="cuda")
@@ -470,7 +470,7 @@ def _decode_layer_chain(oracle_mod, ctx, n, d, layers, seed, early, graph):
 
 @pytest.mark.parametrize("ctx,n,d,graph", [
     ([100, 543, 17, 1, 31], 4, 128, True),                           # static split, bitwise vs the plain call
-    ([int(x) for x in syn.rng(31).integers(300, 900, 384)], 16, 128, True),  # dynamic tail on
+    ([int(x) for x in syn.rng(31).integers(250, 600, 384)], 16, 128, True),  # dynamic tail on (168k pages)
     ([33, 1, 700], 2, 64, False),                                     # eager launches, d = 64
 ])
 def test_decode_early_kv_layer_chain(oracle_mod, ctx, n, d, graph):
@@ -932,8 +932,8 @@ def test_experimental_pair_kernel_parity():
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(here, "test_gpu_parity.py"), "-k",
-                        "prefill and not chunked and not experimental"], env=env, capture_output=True, text=True,
-                       timeout=600)
+                        "prefill and not chunked and not experimental and not shape and not band"],
+                       env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
@@ -951,7 +951,8 @@ def test_prefill_persistence_forced(force):
     here = os.path.dirname(os.path.abspath(__file__))
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(here, "test_gpu_parity.py"), "-k",
-                        "(prefill or chunked or streamed or end_to_end) and not experimental and not forced"],
+                        "(prefill or chunked or streamed or end_to_end or band) and not experimental and not forced "
+                        "and not config4_shape and not config5_shape and not bench_step"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
