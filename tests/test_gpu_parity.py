@@ -306,6 +306,13 @@ def test_decode_nan_poisoned_pool(oracle_mod):
         assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
 
 
+def _takes_dynamic_tail(ctx, n, steps=1):
+    """The decode kernel cuts its last 10 % of pages into dynamic chunks only with >= 64
+    pages per warp (148 SMs x 16 warps): keep the batch above that at its first step."""
+    pages = sum(n * ((c + 1 + 15) // 16) for c in ctx)
+    return pages >= 64 * torch.cuda.get_device_properties(0).multi_processor_count * 16
+
+
 def test_decode_dynamic_chunks(oracle_mod):
     """A batch big enough (>= 64 pages per warp) that the last 10 % of the pages
     are taken dynamically in chunks by whichever warps finish their static range
@@ -313,6 +320,7 @@ def test_decode_dynamic_chunks(oracle_mod):
     and pages each time), and the self-resetting chunk counters must be ready for
     the next launch (the second decode step reuses the workspace)."""
     ctx = [int(x) for x in syn.rng(21).integers(200, 500, 512)]  # 181k pages: >= 64 per warp of 2368
+    assert _takes_dynamic_tail(ctx, 16)
     side, table, cur, errs = run_decode(oracle_mod, ctx, 16, 128, seed=21, steps=2)
     assert max(errs) <= WARN, errs
     assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
@@ -325,6 +333,7 @@ def test_decode_dynamic_chunks_ragged_d64(oracle_mod):
     g = syn.rng(22)
     ctx = [int(x) for x in g.integers(0, 600, 700)]
     ctx[:40] = [0] * 10 + [1] * 10 + [15] * 10 + [16] * 10
+    assert _takes_dynamic_tail(ctx, 24)
     side, table, cur, errs = run_decode(oracle_mod, ctx, 24, 64, seed=22, steps=2, fragment=7)
     assert max(errs) <= WARN, errs
     assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
@@ -346,6 +355,7 @@ def test_decode_workspace_reused_across_batch_shapes(oracle_mod):
     ]
     need = max(ds.ds_decode_workspace_bytes(len(c), n, d, max(c) + 2) for c, n, d in calls)
     ws = torch.zeros(need // 4 + 4, dtype=torch.float32, device="cuda")
+    assert [_takes_dynamic_tail(c, n) for c, n, _ in calls] == [True, True, False, True, True]
     for i, (ctx, n, d) in enumerate(calls):
         _, _, _, errs = run_decode(oracle_mod, ctx, n, d, seed=40 + i, steps=2, ws=ws)
         assert max(errs) <= WARN, (i, errs)
@@ -479,6 +489,7 @@ def test_decode_early_kv_layer_chain(oracle_mod, ctx, n, d, graph):
     appends land, and — where no dynamic chunks make the merge order vary — the
     bytes equal those of the plain call."""
     layers = 4
+    assert len(ctx) < 100 or _takes_dynamic_tail(ctx, n)
     outs, side, table, refs = _decode_layer_chain(oracle_mod, ctx, n, d, layers, 41, True, graph)
     cur = [c + 1 for c in ctx]
     for layer in range(layers):
