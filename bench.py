@@ -987,10 +987,11 @@ def run_ds(args):
         comp["decode_attn_us_per_launch"] = avg_ms * 1e3
         comp["decode_graphs"] = eng.graphs is not None
     roofline = None  # the dominant kernel of this rank's step
-    traffic = ncu_traffic(args, w, "decode_kernel")
+    dec_name = ds.ds_decode_kernel(w.B, w.n) if eng.dc else "decode_kernel"
+    traffic = ncu_traffic(args, w, dec_name)
     if dec_kernel:
         achieved = dec_kernel[0] / (dec_kernel[1] / 1e3) / 1e9
-        roofline = {"kernel": "ds_decode_attn (decode_kernel, split merge fused)", "bound": "hbm",
+        roofline = {"kernel": f"ds_decode_attn ({dec_name}, split merge fused)", "bound": "hbm",
                     "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                     "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)",
@@ -1037,12 +1038,21 @@ def run_ds(args):
         decs = [c for c in objs if "decode_attn_GBps" in c]
         if decs:  # the decode kernel dominates the job; report it from the first decode rank
             d0 = decs[0]
-            line["roofline"] = {"kernel": "ds_decode_attn (decode_kernel, split merge fused)", "bound": "hbm",
+            line["roofline"] = {"kernel": f"ds_decode_attn ({ds.ds_decode_kernel(w.B, w.n)}, split merge fused)",
+                                "bound": "hbm",
                                 "achieved": d0["decode_attn_GBps"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
                                 "frac": d0["decode_attn_GBps"] / peaks["hbm_gbs"], "traffic": None, "peak_note": DECODE_PEAK_NOTE,
                                 "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if os.environ.get("DS_DECODE_TRACE_OUT"):  # -DDS_TRACE builds only: the last decode launch's warp timeline
+        import ctypes
+        import numpy as np
+        f = ctypes.CDLL(ds.LIB_PATH).ds_debug_decode_trace
+        f.argtypes = [ctypes.c_void_p, ctypes.c_int]
+        buf = np.zeros(f(None, 0), np.uint64)
+        f(buf.ctypes.data, 0)
+        np.save(os.environ["DS_DECODE_TRACE_OUT"], buf)
     if comm is not None:
         comm.close()
     if world > 1:

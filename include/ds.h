@@ -216,9 +216,20 @@ ds_status ds_prefill_attn_chunked(const void *q, const void *k, const void *v, v
  * Work split: the (seq, head, page) space is cut into equal page ranges, one
  * per warp of a persistent grid; a pair that straddles ranges is merged from
  * its partials (m, l, o) with the log-sum-exp rule (a8), inside the same launch.
+ * (Opt-in, environment DS_DEC_PAIRS=k read once per process: from k pairs per SM
+ * on, each pair is streamed by one CTA that takes pairs from a counter in the
+ * workspace and merges its warps' partials in shared memory; see decode.cu.)
+ * Where pages are assigned dynamically (the last 10 % of the pages of big
+ * launches; the pair counter) the grouping of pages into partials may differ from
+ * call to call, so results agree to fp32 rounding of the merge, not bit for bit;
+ * fixed-assignment launches are bitwise reproducible.
  * Errors: DS_ERR_INVALID_ARG, DS_ERR_CUDA. */
 size_t ds_decode_workspace_bytes(int32_t num_seqs, int32_t n_loc, int32_t head_dim,
                                  int32_t max_cache_len);
+/* ds_decode_kernel — the name of the kernel ds_decode_attn launches for this batch
+ * shape on the current device ("decode_pairs_kernel" or "decode_kernel"; a static
+ * string, never NULL), for profilers and reports. No device work. */
+const char *ds_decode_kernel(int32_t num_seqs, int32_t n_loc);
 ds_status ds_decode_attn(const void *q, const void *k_new, const void *v_new, void *out,
                          const ds_kv_cache *cache, int32_t layer,
                          const int32_t *block_table, int32_t max_blocks_per_seq,
@@ -238,7 +249,8 @@ ds_status ds_decode_attn(const void *q, const void *k_new, const void *v_new, vo
  *   that only produces q/k_new/v_new. (The kernel before that one has always
  *   finished: an early call lets its successor start only after its own wait.)
  *   A host copy ahead of the call is always safe (it ends the overlap). The
- *   results are identical with and without the flag.
+ *   flag changes no arithmetic (results as without it, up to the dynamic
+ *   assignment noted above).
  * Errors: as ds_decode_attn; DS_ERR_INVALID_ARG for unknown flag bits. */
 #define DS_DECODE_EARLY_KV 1u
 ds_status ds_decode_attn_ex(const void *q, const void *k_new, const void *v_new, void *out,

@@ -29,6 +29,7 @@ BLOCK_SIZE = 16
 EXPORTED = (
     "ds_last_error", "ds_build_info", "ds_pool_create", "ds_pool_destroy", "ds_pool_num_free",
     "ds_block_table", "ds_prefill_attn", "ds_decode_workspace_bytes", "ds_decode_attn", "ds_decode_attn_ex",
+    "ds_decode_kernel",
     "ds_kv_staging_bytes", "ds_kv_pack", "ds_kv_unpack", "ds_comm_get_unique_id", "ds_comm_init",
     "ds_comm_destroy", "ds_kv_migrate_staging_bytes", "ds_kv_migrate", "ds_ipc_export_mem", "ds_ipc_open_mem",
     "ds_ipc_close_mem", "ds_event_create_ipc", "ds_event_open_ipc", "ds_event_record", "ds_event_wait",
@@ -68,6 +69,7 @@ def _load():
         "ds_prefill_attn_chunked": ([P, P, P, P, P, P, i32, i32, i32, i32, cache_p, i32, P, i32, f32, P],
                                     ctypes.c_int),
         "ds_decode_workspace_bytes": ([i32, i32, i32, i32], sz),
+        "ds_decode_kernel": ([i32, i32], ctypes.c_char_p),
         "ds_decode_attn": ([P, P, P, P, cache_p, i32, P, i32, P, i32, i32, f32, P, sz, P], ctypes.c_int),
         "ds_decode_attn_ex": ([P, P, P, P, cache_p, i32, P, i32, P, i32, i32, f32, P, sz, ctypes.c_uint32, P],
                               ctypes.c_int),
@@ -313,6 +315,11 @@ def ds_prefill_attn_chunked(q, k, v, out, cu_seqlens, prefix_lens, max_chunk_len
 
 
 # --------------------------------------------------------------------- a7 + a8
+def ds_decode_kernel(num_seqs: int, n_loc: int) -> str:
+    """name of the kernel ds_decode_attn launches for this batch shape"""
+    return _lib.ds_decode_kernel(num_seqs, n_loc).decode()
+
+
 def ds_decode_workspace_bytes(num_seqs: int, n_loc: int, head_dim: int, max_cache_len: int) -> int:
     return int(_lib.ds_decode_workspace_bytes(num_seqs, n_loc, head_dim, max_cache_len))
 

@@ -309,6 +309,10 @@ extern "C" ds_status ds_prefill_attn_chunked(const void *q, const void *k, const
   return DS_OK;
 }
 
+extern "C" const char *ds_decode_kernel(int32_t num_seqs, int32_t n_loc) {
+  return decode_uses_pairs(num_seqs, n_loc, device_sms()) ? "decode_pairs_kernel" : "decode_kernel";
+}
+
 extern "C" size_t ds_decode_workspace_bytes(int32_t num_seqs, int32_t n_loc, int32_t head_dim,
                                             int32_t max_cache_len) {
   if (num_seqs <= 0 || n_loc <= 0 || (head_dim != 64 && head_dim != 128) || max_cache_len < 0) return 0;

@@ -5,6 +5,13 @@
 // whole cached K/V once per step). Reading R9: the new token's K/V are appended
 // at position c before attending, so the step attends c+1 tokens.
 //
+// Two kernels, one computation (launch_decode picks; decode_uses_pairs):
+//  * decode_kernel (the default), below;
+//  * decode_pairs_kernel (opt-in, DS_DEC_PAIRS): each (sequence, head) pair is
+//    streamed by one CTA, its 16 warps taking the pair's pages round-robin, the
+//    warps' partials merged in shared memory; CTAs take pairs from a counter, so
+//    the launch ends within about one pair's streaming time (see its comment).
+//
 // B200 design (HBM-bound; no tensor cores — every cached element is used once):
 //  * persistent grid of one 16-warp CTA per SM; the (sequence, head, page) space
 //    is flattened and cut into equal contiguous page ranges, one per warp, so
@@ -31,6 +38,8 @@
 //    the opening page burst overlaps the previous kernel's drain;
 //  * the append (i) is fused: the warp that owns the page holding position c
 //    stores k_new/v_new into it and uses them from global memory for token c.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -83,6 +92,18 @@ struct DecCfg {
   static constexpr int kBarOff = kDoneOff + 8;
   static constexpr int kSmem = kBarOff + kWarps * kSlots * 8;
 };
+
+// the consumer's wait for a page slot (A/B knob DS_DEC_WAIT_NS: > 0 adds a suspend-
+// time hint, so waiting lanes sleep instead of spinning)
+#ifndef DS_DEC_WAIT_NS
+#define DS_DEC_WAIT_NS 0
+#endif
+DS_DEVICE void page_wait(uint64_t *bar, uint32_t parity) {
+  if (DS_DEC_WAIT_NS > 0)
+    mbar_wait_sleep(bar, parity, DS_DEC_WAIT_NS);
+  else
+    mbar_wait(bar, parity);
+}
 
 // f32 = bf16 * bf16 + f32 in one instruction (sm_100 FHFMA.BF16, operands read
 // straight from either half of a packed register; the bf16 x bf16 product is exact)
@@ -563,8 +584,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) decode_kernel(const D
       const size_t r2 = ((size_t)cq.b * n + cq.h) * D + (lane % TPG) * 8;
       *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>((kv ? a.v_new : a.k_new) + r2);
     }
-    mbar_wait(&wbar[sk], (int)((hk / C::kSlots) & 1));
-    mbar_wait(&wbar[sv], (int)(((hk + 1) / C::kSlots) & 1));
+    page_wait(&wbar[sk], (int)((hk / C::kSlots) & 1));
+    page_wait(&wbar[sv], (int)(((hk + 1) / C::kSlots) & 1));
 #ifdef DS_TRACE
     if (xc == 0) DTRACE(2, gtimer());
 #endif
@@ -654,6 +675,318 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) decode_kernel(const D
   }
 }
 
+
+// ------------------------------------------------------------------ pair streaming
+// decode_pairs_kernel: the same computation as decode_kernel, with another work
+// split. Every (sequence, head) pair is streamed by ONE CTA, all 16 of its warps at
+// once: the CTA's pairs form one page stream and warp w takes stream pages w, w + 16,
+// w + 32, ... (so each warp holds a partial (m, l, o) of every pair it touched); the
+// partials of a pair meet in shared memory and the warp that publishes the last one
+// merges them (a8) and writes `out`. The CTA takes its pairs one at a time from a
+// global counter (its first pair is blockIdx.x), so no pair is split across CTAs —
+// no global partials or tickets — and the launch ends within about one pair's
+// streaming time (~6 us at 544 tokens with the SM's whole ring behind one pair)
+// instead of one dynamic chunk of one warp (8 pages at ~3 GB/s per warp: the ~12-20
+// us spread of warp finish times of decode_kernel, profiles/r01/decode_trace_*.txt).
+// Used when the batch has enough pairs to keep every SM busy (host: launch_decode).
+constexpr int kPU = 4;  // pairs whose partials can be in shared memory at once
+// pair descriptors in flight: more than twice the units a warp's producer can run
+// ahead of the slowest consumer (2 pages x 16 warps of 1-page pairs), so the
+// publisher never waits on the warp that asks for a descriptor
+constexpr int kPD = 64;
+// descriptors published beyond the one asked for: every pair a CTA holds when the
+// counter runs out is one more pair it streams while others are done. 0 measured best
+// (B = 128 x 544 tokens: 211.7 us vs 212.6 with 1 and 220.3 with 2; the take of the
+// next pair is made when the first warp's producer reaches it, ~4 us before the CTA's
+// consumers do, which hides its ~2 us; profiles/r02/decode_pairs_ab.txt)
+#ifndef DS_DEC_PAIR_LOOKAHEAD
+#define DS_DEC_PAIR_LOOKAHEAD 0
+#endif
+constexpr int kPairLookahead = DS_DEC_PAIR_LOOKAHEAD;
+
+template <int D>
+struct PairCfg {
+  static constexpr int kPageBytes = 16 * D * 2;
+  static constexpr int kSlots = DecCfg<D>::kSlots;
+  static constexpr int kRingBytes = kWarps * kSlots * kPageBytes;
+  static constexpr int kRow = D + 4;                           // o[D], m, l, pad (floats)
+  static constexpr int kPartOff = kRingBytes;                  // float[kPU][kWarps][kRow]
+  static constexpr int kDescOff = kPartOff + kPU * kWarps * kRow * 4;  // int4[kPD]: pair, npg, sbeg, c
+  static constexpr int kCtlOff = kDescOff + kPD * 16;          // int[16], see Ctl
+  static constexpr int kWuOff = kCtlOff + 16 * 4;              // int[kWarps]: unit each warp's consumer is on
+  static constexpr int kBarOff = kWuOff + kWarps * 4;
+  static constexpr int kSmem = kBarOff + kWarps * kSlots * 8;
+};
+enum { CT_SEQ = 0, CT_LOCK = 1, CT_SBEG = 2, CT_END = 3, CT_DONE = 4, CT_GEN = 8 /* [kPU] */, CT_CNT = 12 /* [kPU] */ };
+
+template <int D>
+__global__ void __launch_bounds__(kWarps * 32, 1) decode_pairs_kernel(const DecodeArgs a) {
+  using C = PairCfg<D>;
+  constexpr int TPG = D / 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int dpart = lane % TPG;
+  const int n = a.n_loc;
+  const int num_pairs = a.num_seqs * n;
+  float *part = reinterpret_cast<float *>(smem + C::kPartOff);
+  int4 *desc = reinterpret_cast<int4 *>(smem + C::kDescOff);
+  volatile int *ctl = reinterpret_cast<volatile int *>(smem + C::kCtlOff);
+  volatile int *wunit = reinterpret_cast<volatile int *>(smem + C::kWuOff);
+  uint64_t *wbar = reinterpret_cast<uint64_t *>(smem + C::kBarOff) + warp * C::kSlots;
+  uint8_t *ring = smem + warp * C::kSlots * C::kPageBytes;
+  int *counter = a.dyn + 2, *ctas_done = a.dyn + 3;
+
+  const bool early = a.early_kv != 0;
+  if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
+  DTRACE(0, gtimer());
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 16; ++k) ctl[k] = 0;
+    // unit 0 is static (no counter access before the PDL wait)
+    const int p0 = blockIdx.x;
+    if (p0 < num_pairs) {
+      const int c = a.cache_lens[p0 / n], npg = npages_of(c);
+      desc[0] = make_int4(p0, npg, 0, c);
+      ctl[CT_SBEG] = npg;
+    } else {
+      desc[0] = make_int4(-1, 0, 0, 0);
+      ctl[CT_END] = 1;
+    }
+    ctl[CT_SEQ] = 1;
+  }
+  if (lane == 0) {
+    for (int s = 0; s < C::kSlots; ++s) mbar_init(&wbar[s], 1);
+    wunit[warp] = 0;
+  }
+  fence_barrier_init();
+  __syncthreads();
+  DTRACE(1, gtimer());
+
+  // descriptor d (lane 0 of any warp): published in order by whoever holds the lock;
+  // slot d % kPD is rewritten only when every warp's consumer is past unit d - kPD
+  bool past_wait = !early;
+  // (every wait below backs off with __nanosleep: under the power cap a spinning
+  // warp costs SM clock — the first version's tight CAS loop on the lock measured
+  // 1556 vs 1620 MHz and a slower step in bench.py than the page-range kernel)
+  auto need_desc = [&](int d) {
+    while (ctl[CT_SEQ] <= d) {
+      if (ctl[CT_LOCK] != 0 || atomicCAS(const_cast<int *>(&ctl[CT_LOCK]), 0, 1) != 0) {
+        __nanosleep(128);
+        continue;
+      }
+      int seq = ctl[CT_SEQ];
+      while (seq <= d + kPairLookahead && !ctl[CT_END]) {
+        int lo = 0x7fffffff;
+        for (int w = 0; w < kWarps; ++w) lo = min(lo, wunit[w]);
+        if (lo <= seq - kPD) break;  // descriptor slot still in use
+        const int pr = (int)gridDim.x + atomicAdd(counter, 1);
+        if (pr >= num_pairs) {
+          desc[seq % kPD] = make_int4(-1, 0, 0, 0);
+          ctl[CT_END] = 1;
+        } else {
+          const int c = a.cache_lens[pr / n], npg = npages_of(c), sb = ctl[CT_SBEG];
+          desc[seq % kPD] = make_int4(pr, npg, sb, c);
+          ctl[CT_SBEG] = sb + npg;
+        }
+        __threadfence_block();
+        ctl[CT_SEQ] = ++seq;
+      }
+      __threadfence_block();
+      atomicExch(const_cast<int *>(&ctl[CT_LOCK]), 0);
+    }
+  };
+  auto read_desc = [&](int d) {
+    const volatile int *v = reinterpret_cast<volatile int *>(&desc[d % kPD]);
+    return make_int4(v[0], v[1], v[2], v[3]);
+  };
+
+  const size_t page_elems = 16 * D;
+  const size_t kv_stride = (size_t)a.num_blocks * n * page_elems;
+  const uint16_t *layer_base = a.cache + (size_t)a.layer * 2 * kv_stride;
+
+  // ---- producer (lane 0): stream pages w, w+16, ... one half-page per issue
+  int ps = warp, pd = 0;
+  int4 pdesc = desc[0];
+  bool prod_done = false;
+  int64_t h_issued = 0;
+  const uint16_t *cur_page = nullptr;
+  // false: the stream has ended (or, before the PDL wait, this warp's next page is past unit 0)
+  auto prod_locate = [&]() -> bool {
+    while (pdesc.x >= 0 && ps >= pdesc.z + pdesc.y) {
+      if (!past_wait) return false;
+      ++pd;
+      need_desc(pd);
+      pdesc = read_desc(pd);
+    }
+    return pdesc.x >= 0;
+  };
+  auto issue = [&]() -> bool {
+    if ((h_issued & 1) == 0) {
+      if (!prod_locate()) return false;
+      const int b = pdesc.x / n, h = pdesc.x - b * n, p = ps - pdesc.z;
+      const int blk = a.block_table[(size_t)b * a.max_blocks + p];
+      cur_page = layer_base + ((size_t)blk * n + h) * page_elems;
+      ps += kWarps;
+    }
+    const int slot = (int)(h_issued % C::kSlots);
+    mbar_arrive_expect_tx(&wbar[slot], C::kPageBytes);
+    bulk_g2s(ring + slot * C::kPageBytes, cur_page + ((h_issued & 1) ? kv_stride : 0), C::kPageBytes, &wbar[slot]);
+    ++h_issued;
+    return true;
+  };
+  if (lane == 0)
+    for (int i = 0; i < C::kSlots && issue(); ++i) {
+    }
+  if (early) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    past_wait = true;
+    __syncwarp();
+    if (lane == 0)  // top up what stopped at unit 0
+      while (h_issued < C::kSlots && issue()) {
+      }
+  }
+
+  // ---- consumer (all lanes)
+  int cs = warp, cd = 0;
+  int4 cdesc = desc[0];
+  bool have = false;  // this warp holds a partial of unit cd
+  uint4 qv;
+  float m = kNegInf, l = 0.f, acc[8];
+  size_t row = 0;
+  // publish the partial of unit u (pair pr, npg pages, stream start sb); the last of
+  // its min(16, npg) contributors merges them and writes out[b][h]
+  auto flush = [&](int u, const int4 &dd) {
+#pragma unroll
+    for (int off = TPG; off < 32; off <<= 1)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], off);
+    const int slot = u % kPU, gen = u / kPU;
+    while (ctl[CT_GEN + slot] < gen) __nanosleep(64);
+    float *mine = part + (slot * kWarps + warp) * C::kRow;
+    if (lane < TPG) {
+      reinterpret_cast<float4 *>(mine + dpart * 8)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      reinterpret_cast<float4 *>(mine + dpart * 8)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      if (lane == 0) {
+        mine[D] = m;
+        mine[D + 1] = l;
+      }
+    }
+    __syncwarp();
+    int t = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      t = atomicAdd(const_cast<int *>(&ctl[CT_CNT + slot]), 1);
+    }
+    t = __shfl_sync(0xffffffffu, t, 0);
+    const int k = min(kWarps, dd.y);
+    if (t != k - 1) return;
+    __threadfence_block();
+    constexpr int PER = D / 32;
+    float mm = kNegInf;
+    for (int j = 0; j < k; ++j) mm = fmaxf(mm, part[(slot * kWarps + (dd.z + j) % kWarps) * C::kRow + D]);
+    float lt = 0.f, ot[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) ot[e] = 0.f;
+    for (int j = 0; j < k; ++j) {
+      const float *pj = part + (slot * kWarps + (dd.z + j) % kWarps) * C::kRow;
+      const float wj = rescale(pj[D], mm);
+      lt = fmaf(pj[D + 1], wj, lt);
+#pragma unroll
+      for (int e = 0; e < PER; ++e) ot[e] = fmaf(pj[lane * PER + e], wj, ot[e]);
+    }
+    const float inv = 1.f / lt;
+    const int b = dd.x / n, h = dd.x - b * n;
+    uint16_t *o = reinterpret_cast<uint16_t *>(a.out) + ((size_t)b * n + h) * D + lane * PER;
+#pragma unroll
+    for (int e = 0; e < PER; e += 2) *reinterpret_cast<uint32_t *>(o + e) = pack_bf16(ot[e] * inv, ot[e + 1] * inv);
+    __syncwarp();
+    if (lane == 0) {
+      ctl[CT_CNT + slot] = 0;
+      __threadfence_block();
+      ctl[CT_GEN + slot] = gen + 1;  // the slot's next pair may publish
+    }
+  };
+  // q of the next pair is loaded when this warp enters a pair (if its descriptor is
+  // out), so the load's latency is not paid every ~2 pages
+  uint4 qn = make_uint4(0u, 0u, 0u, 0u);
+  int qn_pair = -1;
+  auto enter = [&](const int4 &dd) {  // first page of this warp in pair dd.x
+    row = ((size_t)dd.x * D) + dpart * 8;  // pair index b * n + h == dd.x
+    qv = qn_pair == dd.x ? qn : *reinterpret_cast<const uint4 *>(a.q + row);
+    qn_pair = -1;
+    if (ctl[CT_SEQ] > cd + 1) {
+      const int4 nx = read_desc(cd + 1);
+      if (nx.x >= 0) {
+        qn = *reinterpret_cast<const uint4 *>(a.q + (size_t)nx.x * D + dpart * 8);
+        qn_pair = nx.x;
+      }
+    }
+    m = kNegInf;
+    l = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+    have = true;
+  };
+
+  for (int64_t xc = 0;; ++xc) {
+    // locate stream page cs (descriptors were published for this warp's producer)
+    while (cdesc.x >= 0 && cs >= cdesc.z + cdesc.y) {
+      if (have) flush(cd, cdesc);
+      have = false;
+      ++cd;
+      while (ctl[CT_SEQ] <= cd) __nanosleep(64);
+      cdesc = read_desc(cd);
+      if (lane == 0) wunit[warp] = cd;
+    }
+    if (cdesc.x < 0) break;
+    if (!have) enter(cdesc);
+    const int p = cs - cdesc.z, c = cdesc.w;
+    const int b = cdesc.x / n, h = cdesc.x - b * n;
+    const bool last = p == (c >> 4);
+    const int64_t hk = 2 * xc;
+    const int sk = (int)(hk % C::kSlots), sv = (int)((hk + 1) % C::kSlots);
+    if (last && lane < 2 * TPG) {  // (i) fused append of the new token at position c
+      const int kv = lane / TPG;
+      const int blk = a.block_table[(size_t)b * a.max_blocks + p];
+      uint16_t *dst = const_cast<uint16_t *>(layer_base) + kv * kv_stride + ((size_t)blk * n + h) * page_elems +
+                      (size_t)(c & 15) * D + (lane % TPG) * 8;
+      *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>((kv ? a.v_new : a.k_new) + row);
+    }
+    page_wait(&wbar[sk], (int)((hk / C::kSlots) & 1));
+    page_wait(&wbar[sv], (int)(((hk + 1) / C::kSlots) & 1));
+#ifdef DS_TRACE
+    if (xc == 0) DTRACE(2, gtimer());
+#endif
+    const uint8_t *kst = ring + sk * C::kPageBytes, *vst = ring + sv * C::kPageBytes;
+    if (last)
+      consume_page<D, true>(kst, vst, qv, acc, m, l, lane, p * 16, c, a.scale_log2, a.k_new + row, a.v_new + row);
+    else
+      consume_page<D, false>(kst, vst, qv, acc, m, l, lane, p * 16, c, a.scale_log2, nullptr, nullptr);
+    __syncwarp();
+    if (lane == 0 && !prod_done) {
+      fence_proxy_async_smem();
+      if (!issue() || !issue()) prod_done = true;
+    }
+    cs += kWarps;
+  }
+  if (lane == 0) wunit[warp] = 0x7fffffff;
+  DTRACE(3, gtimer());
+#ifdef DS_TRACE
+  {
+    // pages consumed by this warp: count the stream indices it visited
+    DTRACE(4, (unsigned long long)((cs - warp) / kWarps));
+  }
+#endif
+
+  // the last warp of the last CTA resets the counters for the next launch
+  if (lane == 0 && atomicAdd(const_cast<int *>(&ctl[CT_DONE]), 1) == kWarps - 1) {
+    if (atomicAdd(ctas_done, 1) == (int)gridDim.x - 1) {
+      *counter = 0;
+      *ctas_done = 0;
+    }
+  }
+}
+
 }  // namespace
 
 #ifdef DS_TRACE
@@ -706,6 +1039,23 @@ static cudaError_t launch_d(cudaLaunchConfig_t &cfg, const DecodeArgs &a) {
   return cudaLaunchKernelEx(&cfg, decode_kernel<D, kDyn>, a);
 }
 
+bool decode_uses_pairs(int num_seqs, int n_loc, int num_sms) {
+  // pair streaming (decode_pairs_kernel): OPT-IN, DS_DEC_PAIRS=k uses it from k pairs
+  // per SM on (read once). Measured (profiles/r02/decode_pairs_ab.txt): alone it is
+  // 4-5 % faster than decode_kernel from B = 32 to 128 x 544 tokens x 40 heads (3 % at
+  // 256; equal at 4.3 pairs per SM, slower below) — B = 128: 211.6 vs 221.0 us, within
+  // 2 % of trtllm-gen — but inside bench.py's step, where the GPU runs at its power
+  // cap, it is 1.5-2.5 % SLOWER (228-231 vs 225 us per launch, SM clock 1635 vs
+  // 1655-1665 MHz): it executes 19 % more instructions (ncu, B = 128: 122.8 M vs
+  // 102.9 M — every warp enters, flushes and polls for every pair), and under the cap
+  // instructions cost clock. The default stays decode_kernel.
+  static const int pairs_mode = [] {
+    const char *e = getenv("DS_DEC_PAIRS");
+    return e ? atoi(e) : 0;
+  }();
+  return pairs_mode > 0 && kCtasPerSm == 1 && (int64_t)num_seqs * n_loc >= (int64_t)pairs_mode * num_sms;
+}
+
 cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaStream_t stream) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(num_sms * kCtasPerSm);
@@ -718,6 +1068,25 @@ cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaSt
   cfg.numAttrs = 1;
   // dynamic chunks only if the batch can reach the threshold (an upper bound of the
   // page count from max_cache_len; the kernel decides exactly from the lengths)
+  if (decode_uses_pairs(a.num_seqs, a.n_loc, num_sms)) {
+    cfg.gridDim = dim3(num_sms);
+    cudaError_t e;
+    if (head_dim == 128) {
+      static cudaError_t st = cudaFuncSetAttribute(decode_pairs_kernel<128>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, PairCfg<128>::kSmem);
+      if (st != cudaSuccess) return st;
+      cfg.dynamicSmemBytes = PairCfg<128>::kSmem;
+      e = cudaLaunchKernelEx(&cfg, decode_pairs_kernel<128>, a);
+    } else {
+      static cudaError_t st = cudaFuncSetAttribute(decode_pairs_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   PairCfg<64>::kSmem);
+      if (st != cudaSuccess) return st;
+      cfg.dynamicSmemBytes = PairCfg<64>::kSmem;
+      e = cudaLaunchKernelEx(&cfg, decode_pairs_kernel<64>, a);
+    }
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+  }
   const int64_t pmax = (int64_t)a.num_seqs * a.n_loc * npages_of(a.max_cache_len);
   const bool dyn = a.max_chunks > 0 && make_part(pmax, (int64_t)num_sms * kWarpsPerSm, a.max_chunks).NC > 0;
   cudaError_t e;

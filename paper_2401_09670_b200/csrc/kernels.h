@@ -37,6 +37,7 @@ struct DecodeLayout {
 };
 DecodeLayout decode_layout(int num_seqs, int n_loc, int head_dim, int num_sms, int max_cache_len);
 cudaError_t launch_decode(const DecodeArgs &a, int head_dim, int num_sms, cudaStream_t stream);
+bool decode_uses_pairs(int num_seqs, int n_loc, int num_sms);  // decode_pairs_kernel vs decode_kernel
 
 // a4 / a6: page rows <-> staging
 struct KvCopyArgs {

@@ -339,6 +339,74 @@ def test_decode_dynamic_chunks_ragged_d64(oracle_mod):
     assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
 
 
+def _pair_kernel_on(ctx, n):
+    """decode_pairs_kernel is opt-in (DS_DEC_PAIRS=k: from k pairs per SM on, read once
+    per process); its cases run in a child process with it set
+    (test_decode_pairs_kernel_forced) and are skipped elsewhere."""
+    return ds.ds_decode_kernel(len(ctx), n) == "decode_pairs_kernel"
+
+
+def _ragged_pairs_ctx(d):
+    g = syn.rng(71 + d)
+    B = 420 if d == 128 else 210
+    ctx = [int(x) for x in g.integers(0, 2000, B)]
+    ctx[:150] = [int(x) for x in g.choice([0, 1, 15], 150)]
+    ctx[200:220] = [255, 256, 271, 272] * 5
+    return ctx
+
+
+@pytest.mark.parametrize("d", [128, 64])
+def test_decode_pairs_kernel_ragged(oracle_mod, d):
+    """The pair-streaming kernel on a ragged batch: long runs of one-page pairs (c = 0,
+    1, 15: a warp's producer then runs ~24 pairs ahead of its consumer, through the
+    descriptor ring), pairs of 16 and 17 pages (every warp holds a partial; the
+    merges wait on the four shared-memory partial slots) and long pairs up to 2000
+    tokens, over a NaN-poisoned, fragmented pool; two steps on one workspace (the
+    pair counter must reset itself)."""
+    n = 2 if d == 128 else 4
+    ctx = _ragged_pairs_ctx(d)
+    if not _pair_kernel_on(ctx, n):
+        pytest.skip("decode_pairs_kernel is off in this process (see test_decode_pairs_kernel_forced)")
+    side, table, cur, errs = run_decode(oracle_mod, ctx, n, d, seed=73, steps=2, fragment=3, poison=True)
+    assert max(errs) <= WARN, errs
+    assert pages_match(to_bits(side.cache.tensor), side.opool, 0, cur, table)
+
+
+def test_decode_pairs_kernel_early_kv_chain(oracle_mod):
+    """The pair-streaming kernel in a CUDA-graph layer loop with DS_DECODE_EARLY_KV:
+    before the PDL wait a CTA may only stream its static first pair (the pair
+    counter is read after it); every layer matches the oracle and its appends land."""
+    ctx = [int(x) for x in syn.rng(75).integers(20, 300, 160)]
+    n, d, layers = 2, 128, 3
+    if not _pair_kernel_on(ctx, n):
+        pytest.skip("decode_pairs_kernel is off in this process (see test_decode_pairs_kernel_forced)")
+    outs, side, table, refs = _decode_layer_chain(oracle_mod, ctx, n, d, layers, 77, True, True)
+    cur = [c + 1 for c in ctx]
+    for layer in range(layers):
+        err = oracle_mod.max_rel_err(to_f64(outs[layer]), refs[layer])
+        assert err <= WARN, (layer, err)
+        assert pages_match(to_bits(side.cache.tensor), side.opool, layer, cur, table)
+
+
+def test_decode_pairs_kernel_forced():
+    """DS_DEC_PAIRS=1 (read once per process) switches ds_decode_attn to
+    decode_pairs_kernel from 1 pair per SM on: its own cases plus the big decode
+    parity cases run in a child process with it."""
+    import os
+    import re
+    import subprocess
+    import sys
+    env = dict(os.environ, DS_DEC_PAIRS="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_parity.py"), "-k",
+                        "decode_pairs_kernel_ragged or decode_pairs_kernel_early or decode_dynamic_chunks or "
+                        "decode_batch256 or config4_shape or decode_parity"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert re.search(r"\b1[0-9] passed", r.stdout) and "skipped" not in r.stdout, r.stdout[-800:]
+
+
 def test_decode_workspace_reused_across_batch_shapes(oracle_mod):
     """ONE workspace, zeroed once, serves calls whose batch, head
     count and head_dim change — growing batches that take the dynamic tail (whose
