@@ -1293,7 +1293,11 @@ def run_e2e(args, eng, w, world, replicas, torch):
         h2d, d2h = int(t[0].item()), int(t[1].item())
     return {"value": replicas * (w.T + w.B * w.out_len) / (ms / 1e3), "unit": "tok/s",
             "h2d_bytes_per_step": h2d // args.e2e_steps, "d2h_bytes_per_step": d2h // args.e2e_steps,
-            "ms_per_step": ms, "steps": args.e2e_steps}
+            "ms_per_step": ms, "steps": args.e2e_steps,
+            # the end-to-end step is bound by the host -> device link: every step's inputs
+            # (each layer's Q/K/V and every decode step's q/k_new/v_new) cross it once
+            "h2d_GBps": (h2d // args.e2e_steps) / (ms / 1e3) / 1e9 / max(1, world),
+            "bound": "host->device copies (pinned H2D; tools/h2d_probe.py measures the link)"}
 
 
 def main():
