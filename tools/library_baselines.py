@@ -22,8 +22,11 @@ the hand-written kernels compare with what a user could call instead on B200":
 
 Each library output is compared with ours (max relative error) so a mis-called
 library cannot report a fake time. Prints one JSON line per (shape, impl).
-The flashinfer trtllm-gen launcher is JIT-built; point FLASHINFER_WORKSPACE_BASE at
-a prebuilt cache (tools/gpu_library_baselines.sh builds it on the CPU host first)."""
+The flashinfer trtllm-gen launcher is JIT-built: tools/build_flashinfer_fmha.sh builds it
+on the CPU host into .fi_ws/; export FLASHINFER_WORKSPACE_BASE=$PWD/.fi_ws and
+FLASHINFER_CUDA_ARCH_LIST=10.0a on the box. DS_SUSTAINED_S=s also times each decode
+shape after s seconds of back-to-back launches (the power-capped steady state of
+bench.py's step; short runs measure boost clocks)."""
 import argparse
 import json
 import math
@@ -39,6 +42,7 @@ import torch
 import paper_2401_09670_b200 as ds
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SUSTAINED = float(os.environ.get("DS_SUSTAINED_S", "0"))  # decode: also time after this many seconds of load
 try:
     PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
 except OSError:
@@ -81,6 +85,39 @@ def timed(run, reps, rot, graph=True):
     e1.record()
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps / 1e3, False
+
+
+def timed_sustained(run, rot, seconds):
+    """device time per call when the GPU has been busy for `seconds` (power-capped
+    steady state, as inside bench.py's step): replay a graph of `rot` calls back to back,
+    time the second half"""
+    for r in range(rot):
+        run(r)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for r in range(rot):
+                run(r)
+    torch.cuda.current_stream().wait_stream(s)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    n = max(2, int(seconds / (e0.elapsed_time(e1) / 1e3)))
+    for _ in range(n // 2):
+        g.replay()
+    e0.record()
+    for _ in range(n - n // 2):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / ((n - n // 2) * rot) / 1e3
 
 
 def relerr(a, b):
@@ -247,6 +284,10 @@ def decode_shape(B, ctx, n, d, impls, layers=8):
             t, graphed = timed(run, 5 * layers, layers)
             rec.update({"us": t * 1e6, "GBps": byts / t / 1e9, "frac_hbm": byts / t / 1e9 / PEAKS["hbm_gbs"],
                         "graph": graphed})
+            if SUSTAINED > 0 and graphed:
+                ts = timed_sustained(run, layers, SUSTAINED)
+                rec.update({"us_sustained": ts * 1e6, "GBps_sustained": byts / ts / 1e9,
+                            "sustained_s": SUSTAINED})
         except Exception as e:  # noqa: BLE001
             rec["error"] = f"{type(e).__name__}: {str(e)[:300]}"
             traceback.print_exc(file=sys.stderr)
@@ -260,6 +301,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--what", default="both", help="both | prefill | decode")
     p.add_argument("--impls", default="ours,fa2,fa4,trtllm,vllm_pa2")
+    p.add_argument("--batches", default="16,64,128,256", help="decode batch sizes")
     a = p.parse_args()
     impls = a.impls.split(",")
     torch.cuda.set_device(0)
@@ -272,7 +314,7 @@ def main():
             torch.cuda.empty_cache()
     if a.what in ("both", "decode"):
         di = [i for i in impls if i in ("ours", "trtllm", "vllm_pa2", "fa4")]
-        for B in (16, 64, 128, 256):
+        for B in [int(x) for x in a.batches.split(",")]:
             decode_shape(B, 544, 40, 128, di)
             torch.cuda.empty_cache()
 
