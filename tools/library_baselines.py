@@ -194,6 +194,10 @@ def prefill_shape(lens, n, d, impls, reps=20, rot=4):
             rec.update({"us": t * 1e6, "tflops": flops / t / 1e12,
                         "frac_tensor_peak": flops / t / 1e12 / PEAKS["bf16_tflops"], "frac_attainable": roof / t,
                         "graph": graphed})
+            if SUSTAINED > 0 and graphed:
+                ts = timed_sustained(run, rot, SUSTAINED)
+                rec.update({"us_sustained": ts * 1e6, "tflops_sustained": flops / ts / 1e12,
+                            "sustained_s": SUSTAINED})
         except Exception as e:  # noqa: BLE001
             rec["error"] = f"{type(e).__name__}: {str(e)[:300]}"
             traceback.print_exc(file=sys.stderr)
@@ -302,6 +306,7 @@ def main():
     p.add_argument("--what", default="both", help="both | prefill | decode")
     p.add_argument("--impls", default="ours,fa2,fa4,trtllm,vllm_pa2")
     p.add_argument("--batches", default="16,64,128,256", help="decode batch sizes")
+    p.add_argument("--shapes", default="128x512,16x512,16x2048,4x4096,mix5", help="prefill shapes")
     a = p.parse_args()
     impls = a.impls.split(",")
     torch.cuda.set_device(0)
@@ -309,7 +314,10 @@ def main():
         pi = [i for i in impls if i in ("ours", "fa2", "fa4", "trtllm")]
         rng = np.random.default_rng(0)
         mix5 = [int(x) for x in rng.integers(1792, 1921, size=8)]
-        for lens, n in (([512] * 128, 40), ([512] * 16, 40), ([2048] * 16, 40), ([4096] * 4, 40), (mix5, 24)):
+        shapes = {"128x512": ([512] * 128, 40), "16x512": ([512] * 16, 40), "16x2048": ([2048] * 16, 40),
+                  "4x4096": ([4096] * 4, 40), "mix5": (mix5, 24)}
+        for key in a.shapes.split(","):
+            lens, n = shapes[key]
             prefill_shape(lens, n, 128, pi)
             torch.cuda.empty_cache()
     if a.what in ("both", "decode"):
