@@ -520,13 +520,15 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) decode_kernel(const D
     return off;
   };
   int64_t h_issued = 0;
+  int p_slot = 0;  // ring slot of the next half-page
   const uint16_t *cur_page = nullptr;
   auto issue = [&]() -> bool {  // one half-page into the ring; false when nothing is left
     if ((h_issued & 1) == 0) {
       if (pr_x == pr_x1 && !next_range()) return false;
       cur_page = layer_base + next_page() * page_elems;
     }
-    const int slot = (int)(h_issued % C::kSlots);
+    const int slot = p_slot;  // == h_issued % kSlots, kept incrementally (no 64-bit division per issue)
+    if (++p_slot == C::kSlots) p_slot = 0;
     mbar_arrive_expect_tx(&wbar[slot], C::kPageBytes);
     bulk_g2s(ring + slot * C::kPageBytes, cur_page + ((h_issued & 1) ? kv_stride : 0), C::kPageBytes,
              &wbar[slot]);
@@ -572,9 +574,14 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) decode_kernel(const D
   load_pair();
 
   int64_t x = x0, xc = 0;  // page, and pages consumed by this warp so far
+  int c_slot = 0, c_ph = 0;  // consumer's ring slot and phase parity (see below)
   for (;; ++x, ++xc) {
-    const int64_t hk = 2 * xc;
-    const int sk = (int)(hk % C::kSlots), sv = (int)((hk + 1) % C::kSlots);
+    // ring slots and phase parities of this page's half-pages 2 xc, 2 xc + 1, kept
+    // incrementally: the 64-bit divisions by kSlots cost ~20 instructions per page
+    const int sk = c_slot, pk = c_ph;
+    if (++c_slot == C::kSlots) c_slot = 0, c_ph ^= 1;
+    const int sv = c_slot, pv = c_ph;
+    if (++c_slot == C::kSlots) c_slot = 0, c_ph ^= 1;
     const bool last = cq.p == (c >> 4);
     if (last && lane < 2 * TPG) {  // (i) fused append of the new token at position c
       const int kv = lane / TPG;
@@ -584,8 +591,8 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) decode_kernel(const D
       const size_t r2 = ((size_t)cq.b * n + cq.h) * D + (lane % TPG) * 8;
       *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>((kv ? a.v_new : a.k_new) + r2);
     }
-    page_wait(&wbar[sk], (int)((hk / C::kSlots) & 1));
-    page_wait(&wbar[sv], (int)(((hk + 1) / C::kSlots) & 1));
+    page_wait(&wbar[sk], pk);
+    page_wait(&wbar[sv], pv);
 #ifdef DS_TRACE
     if (xc == 0) DTRACE(2, gtimer());
 #endif
@@ -808,6 +815,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_pairs_kernel(const Deco
   int4 pdesc = desc[0];
   bool prod_done = false;
   int64_t h_issued = 0;
+  int p_slot = 0;  // ring slot of the next half-page
   const uint16_t *cur_page = nullptr;
   // false: the stream has ended (or, before the PDL wait, this warp's next page is past unit 0)
   auto prod_locate = [&]() -> bool {
@@ -827,7 +835,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_pairs_kernel(const Deco
       cur_page = layer_base + ((size_t)blk * n + h) * page_elems;
       ps += kWarps;
     }
-    const int slot = (int)(h_issued % C::kSlots);
+    const int slot = p_slot;  // == h_issued % kSlots, kept incrementally (no 64-bit division per issue)
+    if (++p_slot == C::kSlots) p_slot = 0;
     mbar_arrive_expect_tx(&wbar[slot], C::kPageBytes);
     bulk_g2s(ring + slot * C::kPageBytes, cur_page + ((h_issued & 1) ? kv_stride : 0), C::kPageBytes, &wbar[slot]);
     ++h_issued;
@@ -928,6 +937,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_pairs_kernel(const Deco
     have = true;
   };
 
+  int c_slot = 0, c_ph = 0;  // consumer's ring slot and phase parity (see below)
   for (int64_t xc = 0;; ++xc) {
     // locate stream page cs (descriptors were published for this warp's producer)
     while (cdesc.x >= 0 && cs >= cdesc.z + cdesc.y) {
@@ -943,8 +953,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_pairs_kernel(const Deco
     const int p = cs - cdesc.z, c = cdesc.w;
     const int b = cdesc.x / n, h = cdesc.x - b * n;
     const bool last = p == (c >> 4);
-    const int64_t hk = 2 * xc;
-    const int sk = (int)(hk % C::kSlots), sv = (int)((hk + 1) % C::kSlots);
+    // ring slots and phase parities of this page's half-pages 2 xc, 2 xc + 1, kept
+    // incrementally: the 64-bit divisions by kSlots cost ~20 instructions per page
+    const int sk = c_slot, pk = c_ph;
+    if (++c_slot == C::kSlots) c_slot = 0, c_ph ^= 1;
+    const int sv = c_slot, pv = c_ph;
+    if (++c_slot == C::kSlots) c_slot = 0, c_ph ^= 1;
     if (last && lane < 2 * TPG) {  // (i) fused append of the new token at position c
       const int kv = lane / TPG;
       const int blk = a.block_table[(size_t)b * a.max_blocks + p];
@@ -952,8 +966,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_pairs_kernel(const Deco
                       (size_t)(c & 15) * D + (lane % TPG) * 8;
       *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>((kv ? a.v_new : a.k_new) + row);
     }
-    page_wait(&wbar[sk], (int)((hk / C::kSlots) & 1));
-    page_wait(&wbar[sv], (int)(((hk + 1) / C::kSlots) & 1));
+    page_wait(&wbar[sk], pk);
+    page_wait(&wbar[sv], pv);
 #ifdef DS_TRACE
     if (xc == 0) DTRACE(2, gtimer());
 #endif

@@ -2,6 +2,8 @@
 // read (what decode attention does: every cached K/V byte read once) with 16-B
 // vector loads and with 1-D TMA bulk copies into smem, and (b) device-to-device
 // copy (read + write, the MEASURED_PEAKS "copy" figure). 4 GiB buffers, > L2.
+// Usage: hbm_read_bench [MiB] [sustain_seconds] — with a second argument each pattern is
+// also timed after that many seconds back to back (the power-capped steady state).
 #include <cstdio>
 #include <cstdlib>
 #include <cstdint>
@@ -121,6 +123,7 @@ int main(int argc, char **argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const size_t bytes = argc > 1 ? (size_t)atoll(argv[1]) << 20 : 4ull << 30;  // MiB
+  const double sustain_s = argc > 2 ? atof(argv[2]) : 0.0;  // also time each pattern after this long under load
   uint8_t *a, *b;
   unsigned long long *sink;
   cudaMalloc(&a, bytes);
@@ -159,7 +162,29 @@ int main(int argc, char **argv) {
       if (ms < best) best = ms;
     }
     const double moved = (k == 3 ? 2.0 : 1.0) * bytes;
-    printf("%-34s %8.3f ms  %7.1f GB/s\n", names[k], best, moved / best / 1e6);
+    printf("%-34s %8.3f ms  %7.1f GB/s", names[k], best, moved / best / 1e6);
+    if (sustain_s > 0) {  // the same launch back to back for sustain_s seconds; average of the last half
+      const int n = (int)(sustain_s * 1e3 / best);
+      for (int rep = 0; rep < n; ++rep) {
+        if (rep == n / 2) cudaEventRecord(e0);
+        if (k == 0) read_ld<<<sms * 8, 512>>>((const uint4 *)a, bytes / 16, sink);
+        else if (k == 1) read_bulk<16384, 8, false><<<sms, 32, 8 * 16384>>>(a, bytes, sink);
+        else if (k == 2) read_bulk<16384, 8, false><<<sms * 2, 32, 8 * 16384>>>(a, bytes, sink);
+        else if (k == 3) cudaMemcpyAsync(b, a, bytes, cudaMemcpyDeviceToDevice);
+        else if (k == 4) read_bulk<4096, 48, false><<<sms, 32, 48 * 4096>>>(a, bytes, sink);
+        else if (k == 5) read_bulk<4096, 48, true><<<sms, 32, 48 * 4096>>>(a, bytes, sink);
+        else if (k == 6) read_bulk<4096, 24, true><<<sms * 2, 32, 24 * 4096>>>(a, bytes, sink);
+        else if (k == 7) read_warps<3><<<sms, 512, 16 * 3 * 4096>>>(a, bytes, 1, sink);
+        else read_warps<3><<<sms, 512, 16 * 3 * 4096>>>(a, bytes, 40, sink);
+      }
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double per = ms / (n - n / 2);
+      printf("   sustained %.0f s: %8.3f ms  %7.1f GB/s", sustain_s, per, moved / per / 1e6);
+    }
+    printf("\n");
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
