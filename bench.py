@@ -51,7 +51,8 @@ METRIC = "prefill tok/s, decode tok/s/GPU, KV migrate GB/s at 1/2/4/8 B200 vs ro
 # (read + write) figure, so frac can exceed 1 — a pure streaming read of this part
 # reaches 7.1-7.3 TB/s (tools/hbm_read_bench.cu, profiles/r01/hbm_read_bench.txt)
 DECODE_PEAK_NOTE = ("peak = driver-measured copy bandwidth (read+write); decode is ~99.9% reads, whose streaming "
-                    "ceiling measured 7.1-7.3 TB/s on this part (profiles/r01/hbm_read_bench.txt)")
+                    "ceiling measured 7.1-7.3 TB/s on this part, 7.0-7.1 TB/s for its page-ring pattern sustained "
+                    "for 5 s (profiles/r01/hbm_read_bench.txt, profiles/r02/hbm_read_bench_sustained.txt)")
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 NVLINK_GBS = 900.0  # nominal per direction per GPU (770 measured peer copy, B200_PROFILING.md)
