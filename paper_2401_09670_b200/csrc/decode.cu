@@ -70,6 +70,17 @@ constexpr int kWarpsPerSm = kWarps * kCtasPerSm;
 // dynamically (one atomic counter) when their static range is done, so the warps
 // that stream slower (DRAM latency differs per SM) no longer set the launch's end.
 constexpr int kDynPct = DS_DEC_DYN_PCT;
+// below kDynPctSwitch pages per warp the dynamic share is kDynPctLow %: measured in
+// bench.py's power-capped step (config 2, B = 128, ~75 pages per warp) 7 % x 8-page
+// chunks beat 10 % (216.4 vs 220.1 us per launch; 5 %: 217.9, 3 %: 224.4, 0 %: 222.5,
+// 15-20 %: 220.0-220.9, 4-page chunks 223-224), while at B = 256 (~150 pages per
+// warp) 10 % stays best (sustained: 427.3 vs 429.4 us at 7 %; equal at B = 192,
+// ~112 pages per warp). profiles/r02/decode_dyn_share_ab.txt
+#ifndef DS_DEC_DYN_PCT_LOW
+#define DS_DEC_DYN_PCT_LOW 7
+#endif
+constexpr int kDynPctLow = DS_DEC_DYN_PCT_LOW;
+constexpr int kDynPctSwitch = 112;
 constexpr int kChunkPages = DS_DEC_CHUNK;
 #ifndef DS_DEC_DYN_MINPW
 #define DS_DEC_DYN_MINPW 64
@@ -245,7 +256,8 @@ __host__ __device__ inline Part make_part(int64_t P, int64_t Wmax, int64_t max_c
   // only with >= 64 pages per warp (measured: B = 128 and 256 x 544 tokens gain 5-7 %,
   // B <= 64 loses up to 10 %: there the takes, the chunk partials and their merges
   // cost more than the balance gains)
-  if (kDynPct > 0 && P >= kDynMinPagesPerWarp * q.W) dyn = (P * kDynPct / 100) / kChunkPages * kChunkPages;
+  const int64_t pct = P < kDynPctSwitch * q.W ? kDynPctLow : kDynPct;
+  if (kDynPct > 0 && P >= kDynMinPagesPerWarp * q.W) dyn = (P * pct / 100) / kChunkPages * kChunkPages;
   if (dyn > max_chunks * kChunkPages) dyn = max_chunks * kChunkPages;  // workspace bound
   q.P1 = P - dyn;
   q.P = P;
