@@ -109,6 +109,16 @@ struct DecCfg {
 #ifndef DS_DEC_WAIT_NS
 #define DS_DEC_WAIT_NS 0
 #endif
+// the ring's copies and barriers by 32-bit shared-window address, computed once per
+// warp (the generic -> shared conversion per call cost a few instructions per issue)
+DS_DEVICE void expect_tx_s(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+DS_DEVICE void bulk_g2s_s(uint32_t dst, const void *gsrc, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(bar)
+               : "memory");
+}
 DS_DEVICE void page_wait(uint64_t *bar, uint32_t parity) {
   if (DS_DEC_WAIT_NS > 0)
     mbar_wait_sleep(bar, parity, DS_DEC_WAIT_NS);
@@ -480,6 +490,7 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) decode_kernel(const D
   // per-warp ring of kSlots half-stages: slot 2k holds a K page, 2k+1 its V page
   uint8_t *ring = smem + warp * C::kSlots * C::kPageBytes;
   uint64_t *wbar = bars + warp * C::kSlots;
+  const uint32_t ring_s = smem_u32(ring), wbar_s = smem_u32(wbar);
   // per-warp queue of the page ranges this warp streams (its static range, then the
   // dynamic chunks it took), written by the producer lane, read by the whole warp
   int64_t *rq = reinterpret_cast<int64_t *>(smem + C::kRangeOff) + warp * 3 * kRangeQ;
@@ -558,9 +569,9 @@ __global__ void __launch_bounds__(kWarps * 32, kCtasPerSm) decode_kernel(const D
     }
     const int slot = p_slot;  // == h_issued % kSlots, kept incrementally (no 64-bit division per issue)
     if (++p_slot == C::kSlots) p_slot = 0;
-    mbar_arrive_expect_tx(&wbar[slot], C::kPageBytes);
-    bulk_g2s(ring + slot * C::kPageBytes, cur_page + ((h_issued & 1) ? kv_stride : 0), C::kPageBytes,
-             &wbar[slot]);
+    expect_tx_s(wbar_s + slot * 8, C::kPageBytes);
+    bulk_g2s_s(ring_s + slot * C::kPageBytes, cur_page + ((h_issued & 1) ? kv_stride : 0), C::kPageBytes,
+               wbar_s + slot * 8);
     ++h_issued;
     return true;
   };
