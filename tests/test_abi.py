@@ -206,6 +206,26 @@ def test_decode_validation_and_workspace():
     assert call_ex(ds.DS_DECODE_EARLY_KV) == ds.DS_ERR_CUDA  # a valid call, no device here
 
 
+def test_decode_kernel_query():
+    """ds_decode_kernel names the kernel a batch shape gets (no device work): the
+    page-range kernel by default; decode_pairs_kernel only when DS_DEC_PAIRS opts in
+    (read once per process: checked in a child with it set)."""
+    import os
+    import subprocess
+    import sys
+    names = {ds.ds_decode_kernel(b, n) for b in (1, 64, 128, 4096) for n in (1, 40)}
+    expect = {"decode_kernel"} if not os.environ.get("DS_DEC_PAIRS") else {"decode_kernel", "decode_pairs_kernel"}
+    assert names <= expect, names
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import paper_2401_09670_b200 as ds; "
+            "print(ds.ds_decode_kernel(1, 4), ds.ds_decode_kernel(128, 40))")
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=120,
+                       env=dict(os.environ, DS_DEC_PAIRS="4"))
+    assert r.returncode == 0, r.stderr[-2000:]
+    # 4 pairs per SM: 1 x 4 pairs -> page ranges; 128 x 40 = 5120 pairs -> pair streaming
+    assert r.stdout.split() == ["decode_kernel", "decode_pairs_kernel"], r.stdout
+
+
 def test_decode_workspace_holds_the_dynamic_chunks():
     """The workspace grows with the batch's page count once the dynamic tail is on
     (>= 64 pages per warp of the largest grid: 160 SMs x 16 warps): 10 % of the
