@@ -24,7 +24,8 @@ struct DecodeArgs {
   float *workspace;                   // [warps][2][D+4] straddling-pair partials (o, m, l, pad)
   int32_t *tickets;                   // [kDecodeMaxPairs] merge tickets, pair b*n+h (zero between launches)
   float *chunk_rows;                  // [chunks][2][D+4] partials of the dynamically taken chunks
-  int32_t *dyn;                       // [2]: chunk counter, finished warps (zero between launches)
+  int32_t *dyn;                       // [4]: chunk counter, finished CTAs (decode_kernel); pair counter,
+                                      // finished CTAs (decode_pairs_kernel) — zero between launches
   int64_t max_chunks;                 // capacity of chunk_rows
   int32_t max_cache_len;              // bound of cache_lens (host-side kernel choice)
   int32_t early_kv;                   // read lengths / table / pages before the PDL wait
